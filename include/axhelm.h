@@ -1,0 +1,98 @@
+/*
+ * axhelm.h — C ABI of libaxhelm_sm100.so, the B200 (sm_100a) drop-in for the
+ * reference's ax_helm kernel.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg):
+ *   __dace_ax_helm        src/mdg/codegen.py:183-194 (_signature), pinned by
+ *                         tests/test_codegen.py:27-36; ABI order
+ *                         src/mdg/axprogram.py:32-48.
+ *                         Bound by src/mdg/kernelrt.py:77-108 (ctypes) and
+ *                         cabi-harness/src/run.ts:64-74 (koffi).
+ *   axhelm_*              extensions the reference's void ABI lacks
+ *                         (SURVEY §8b): a stream-ordered device entry with an
+ *                         error return and 64-bit element count, and an
+ *                         error/version query.  Gather-scatter and the mesh
+ *                         store have no reference counterpart.
+ *
+ * Data layout: fields are [nel][lx][lx][lx] row-major FP64 (i fastest), the
+ * six matrices [lx][lx] row-major.  lx must lie in [2, 16] (sem.py:36-37).
+ *
+ * Arithmetic modes: AXHELM_STRICT reproduces the reference's strict-fp
+ * operation order bit for bit; AXHELM_FAST fuses multiply-adds (<= 1e-12
+ * normwise from the reference, the tolerance of tests/test_codegen.py:180-187).
+ */
+#ifndef AXHELM_SM100_H
+#define AXHELM_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+#define AXH_RESTRICT __restrict__
+extern "C" {
+#else
+#define AXH_RESTRICT restrict
+#endif
+
+enum axhelm_mode { AXHELM_STRICT = 0, AXHELM_FAST = 1 };
+
+enum axhelm_status {
+  AXHELM_OK = 0,
+  AXHELM_EINVAL = 1,   /* bad lx, negative nel, null pointer */
+  AXHELM_ECUDA = 2,    /* CUDA runtime error (message in last_error) */
+  AXHELM_ENODEV = 3,   /* no usable sm_100 device */
+};
+
+/* The reference ABI, exactly (codegen.py:183-194).  Synchronous: returns
+ * with wd written.  Accepts device pointers (kernel on the calling thread's
+ * default stream) or host pointers, pinned or pageable (chunked,
+ * copy/compute-overlapped staging through the GPU).  The void return has no
+ * error channel: failures are reported by axhelm_last_status(). */
+void __dace_ax_helm(double* AXH_RESTRICT wd, const double* AXH_RESTRICT ud,
+                    const double* AXH_RESTRICT dxd, const double* AXH_RESTRICT dyd,
+                    const double* AXH_RESTRICT dzd, const double* AXH_RESTRICT dxtd,
+                    const double* AXH_RESTRICT dytd, const double* AXH_RESTRICT dztd,
+                    const double* AXH_RESTRICT h1d, const double* AXH_RESTRICT g11d,
+                    const double* AXH_RESTRICT g22d, const double* AXH_RESTRICT g33d,
+                    const double* AXH_RESTRICT g12d, const double* AXH_RESTRICT g13d,
+                    const double* AXH_RESTRICT g23d, int nelv, int lx);
+
+/* Stream-ordered device entry: every pointer is a device pointer; enqueues
+ * the apply on `stream` (a cudaStream_t, NULL = legacy default stream) and
+ * returns without synchronising. */
+int axhelm_apply(double* wd, const double* ud, const double* dxd,
+                 const double* dyd, const double* dzd, const double* dxtd,
+                 const double* dytd, const double* dztd, const double* h1d,
+                 const double* g11d, const double* g22d, const double* g33d,
+                 const double* g12d, const double* g13d, const double* g23d,
+                 int64_t nel, int lx, int mode, void* stream);
+
+/* __dace_ax_helm with an explicit mode and a status return: synchronous,
+ * host or device pointers (per-array), 64-bit element count. */
+int axhelm_apply_sync(double* wd, const double* ud, const double* dxd,
+                      const double* dyd, const double* dzd, const double* dxtd,
+                      const double* dytd, const double* dztd, const double* h1d,
+                      const double* g11d, const double* g22d, const double* g33d,
+                      const double* g12d, const double* g13d, const double* g23d,
+                      int64_t nel, int lx, int mode);
+
+/* Mode used by __dace_ax_helm (default AXHELM_STRICT, or AXHELM_FAST when
+ * the environment variable AXHELM_FP=fast is set at load time). */
+int axhelm_set_mode(int mode);
+int axhelm_get_mode(void);
+
+/* Status of the last call on this thread, and its message. */
+int axhelm_last_status(void);
+const char* axhelm_last_error(void);
+const char* axhelm_version(void);
+
+/* Algorithmic model: bytes = 72*nel*lx^3, flops =
+ * nel*lx^3*(12*lx+18) (sem.py:367-375). */
+int64_t axhelm_bytes_model(int64_t nel, int lx);
+int64_t axhelm_flops_model(int64_t nel, int lx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AXHELM_SM100_H */

@@ -1,0 +1,192 @@
+// ax_helm element kernels for sm_100a (B200), FP64.
+//
+// Operator (reference: /root/reference/pkg/src/mdg/sem.py:300-337, tasklets
+// axprogram.py:159-163 stage 1, :188-192 combine, :229 stage 2):
+//
+//   r[e,k,j,i] = sum_l dxd[l,i] u[e,k,j,l]     s = sum_l dyd[l,j] u[e,k,l,i]
+//   t[e,k,j,i] = sum_l dzd[l,k] u[e,l,j,i]
+//   ur = h1 ((g11 r + g12 s) + g13 t)  us = h1 ((g12 r + g22 s) + g23 t)
+//   ut = h1 ((g13 r + g23 s) + g33 t)
+//   w[e,k,j,i] = sum_l ((dxtd[l,i] ur[e,k,j,l] + dytd[l,j] us[e,k,l,i]) + dztd[l,k] ut[e,l,j,i])
+//                (accumulated term by term, l ascending, from 0.0)
+//
+// Layout in HBM: every field is [nel][lx][lx][lx] row-major, i fastest
+// (sem.py:68-100); the six matrices are [lx][lx] row-major.
+//
+// Two arithmetic modes, chosen at compile time:
+//   Strict (FAST=false): every multiply and add is a separate IEEE-754
+//     round-to-nearest operation (__dmul_rn / __dadd_rn) in exactly the
+//     reference's association, so the output is bit-identical to
+//     mdg.sem.ax_reference and to the reference's strict-fp compiled kernel.
+//   Fast (FAST=true): the same sums with fused multiply-adds; differs from
+//     the reference by FP64 reassociation only (<= 1e-12 normwise).
+//
+// Thread mapping ("k-walk"): one thread per (j,i) column of an element; the
+// thread walks k.  Its u column and its ut column stay in registers, the
+// element's u and the ur/us slices live in shared memory (row stride padded
+// to an odd number of doubles so the row-broadcast reads hit distinct
+// banks).  EPB elements share one CTA so the CTA has >= ~128 threads for
+// every lx.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axb {
+
+struct AxPtrs {
+  double* __restrict__ w;
+  const double* __restrict__ u;
+  const double* __restrict__ dx;
+  const double* __restrict__ dy;
+  const double* __restrict__ dz;
+  const double* __restrict__ dxt;
+  const double* __restrict__ dyt;
+  const double* __restrict__ dzt;
+  const double* __restrict__ h1;
+  const double* __restrict__ g11;
+  const double* __restrict__ g22;
+  const double* __restrict__ g33;
+  const double* __restrict__ g12;
+  const double* __restrict__ g13;
+  const double* __restrict__ g23;
+};
+
+template <int LX>
+struct KCfg {
+  static constexpr int L2 = LX * LX;
+  static constexpr int L3 = LX * LX * LX;
+  // elements per CTA: aim for ~128 threads, at least one element
+  static constexpr int EPB = (L2 >= 128) ? 1 : (128 / L2);
+  static constexpr int NT = EPB * L2;
+  static constexpr int RS = LX | 1;        // padded row stride (doubles)
+  static constexpr int SL = LX * RS;       // slice stride
+  static constexpr int ES = LX * SL;       // element stride in smem
+  static constexpr size_t SMEM = sizeof(double) * (6 * L2 + 3 * EPB * ES);
+};
+
+// acc + a*b with the requested rounding discipline
+template <bool FAST>
+__device__ __forceinline__ double madd(double acc, double a, double b) {
+  if constexpr (FAST) {
+    return fma(a, b, acc);
+  } else {
+    return __dadd_rn(acc, __dmul_rn(a, b));
+  }
+}
+
+// h * ((ga*r + gb*s) + gc*t)
+template <bool FAST>
+__device__ __forceinline__ double combine(double h, double ga, double gb, double gc,
+                                          double r, double s, double t) {
+  if constexpr (FAST) {
+    return h * fma(gc, t, fma(gb, s, ga * r));
+  } else {
+    return __dmul_rn(h, __dadd_rn(__dadd_rn(__dmul_rn(ga, r), __dmul_rn(gb, s)),
+                                  __dmul_rn(gc, t)));
+  }
+}
+
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_stream(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// v1 k-walk kernel: one CTA per EPB elements.
+template <int LX, bool FAST>
+__global__ void __launch_bounds__(KCfg<LX>::NT)
+ax_kwalk(const AxPtrs A, const int64_t nel) {
+  using C = KCfg<LX>;
+  constexpr int L2 = C::L2, L3 = C::L3, RS = C::RS, SL = C::SL, ES = C::ES;
+  extern __shared__ double smem[];
+  double* sD = smem;                    // [6][LX][LX]
+  double* sU = sD + 6 * L2;             // [EPB][LX][LX][RS]
+  double* sR = sU + C::EPB * ES;
+  double* sS = sR + C::EPB * ES;
+
+  const int tid = threadIdx.x;
+  for (int q = tid; q < L2; q += C::NT) {
+    sD[0 * L2 + q] = A.dx[q];
+    sD[1 * L2 + q] = A.dy[q];
+    sD[2 * L2 + q] = A.dz[q];
+    sD[3 * L2 + q] = A.dxt[q];
+    sD[4 * L2 + q] = A.dyt[q];
+    sD[5 * L2 + q] = A.dzt[q];
+  }
+  const int el = tid / L2;
+  const int p = tid - el * L2;
+  const int j = p / LX;
+  const int i = p - j * LX;
+  const int64_t e = (int64_t)blockIdx.x * C::EPB + el;
+  const bool active = e < nel;
+  const int64_t gbase = e * L3 + p;  // + k*L2
+  double* eU = sU + el * ES;
+  double* eR = sR + el * ES;
+  double* eS = sS + el * ES;
+
+  double ureg[LX];
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    ureg[k] = active ? ldg_stream(A.u + gbase + k * L2) : 0.0;
+    eU[k * SL + j * RS + i] = ureg[k];
+  }
+  __syncthreads();
+
+  double dxr[LX], dyr[LX];
+#pragma unroll
+  for (int l = 0; l < LX; ++l) {
+    dxr[l] = sD[0 * L2 + l * LX + i];
+    dyr[l] = sD[1 * L2 + l * LX + j];
+  }
+
+  double utr[LX];
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    const int64_t g = gbase + k * L2;
+    double h = 0, a11 = 0, a22 = 0, a33 = 0, a12 = 0, a13 = 0, a23 = 0;
+    if (active) {
+      h = ldg_stream(A.h1 + g);
+      a11 = ldg_stream(A.g11 + g);
+      a22 = ldg_stream(A.g22 + g);
+      a33 = ldg_stream(A.g33 + g);
+      a12 = ldg_stream(A.g12 + g);
+      a13 = ldg_stream(A.g13 + g);
+      a23 = ldg_stream(A.g23 + g);
+    }
+    double r = 0.0, s = 0.0, t = 0.0;
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      r = madd<FAST>(r, dxr[l], eU[k * SL + j * RS + l]);
+      s = madd<FAST>(s, dyr[l], eU[k * SL + l * RS + i]);
+      t = madd<FAST>(t, sD[2 * L2 + l * LX + k], ureg[l]);
+    }
+    eR[k * SL + j * RS + i] = combine<FAST>(h, a11, a12, a13, r, s, t);
+    eS[k * SL + j * RS + i] = combine<FAST>(h, a12, a22, a23, r, s, t);
+    utr[k] = combine<FAST>(h, a13, a23, a33, r, s, t);
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int l = 0; l < LX; ++l) {
+    dxr[l] = sD[3 * L2 + l * LX + i];
+    dyr[l] = sD[4 * L2 + l * LX + j];
+  }
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    double w = 0.0;
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      w = madd<FAST>(w, dxr[l], eR[k * SL + j * RS + l]);
+      w = madd<FAST>(w, dyr[l], eS[k * SL + l * RS + i]);
+      w = madd<FAST>(w, sD[5 * L2 + l * LX + k], utr[l]);
+    }
+    if (active) stg_stream(A.w + gbase + k * L2, w);
+  }
+}
+
+}  // namespace axb

@@ -1,0 +1,24 @@
+// Internal (non-ABI) declarations shared by the translation units of
+// libaxhelm_sm100.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ax_kernels.cuh"
+
+namespace axb {
+
+int set_status(int st, const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+int default_mode();
+
+// enqueue one apply over device pointers (no validation)
+cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st);
+
+// __dace_ax_helm body: classify the 15 pointers (device / pinned host /
+// pageable host) and run the apply synchronously, staging host data through
+// the GPU in copy/compute-overlapped chunks.
+int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int mode);
+
+}  // namespace axb

@@ -1,0 +1,149 @@
+// Host-pointer path of __dace_ax_helm (reference: kernelrt.py:95-106 and
+// cabi-harness/src/run.ts:64-74 both pass HOST buffers through the ABI).
+//
+// The apply is split into element chunks (~1 Mi points, 8 MiB per field)
+// that cycle through NS device slots on NS streams: chunk c's host->device
+// copies, its kernel and its device->host copy of w are enqueued on stream
+// c % NS, so the H2D copy engine, the SMs and the D2H copy engine work on
+// three different chunks at once.  Arrays that are already device (or
+// managed) memory are used in place, so mixed host/device argument sets work.
+// Pinned host buffers are DMA'd directly; pageable ones go through the
+// driver's staging copy.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "../../include/axhelm.h"
+#include "ax_launch.h"
+
+namespace axb {
+
+namespace {
+
+enum Kind { DEV = 0, PINNED = 1, PAGEABLE = 2 };
+
+Kind classify(const void* p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error
+    return PAGEABLE;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return DEV;
+  if (a.type == cudaMemoryTypeHost) return PINNED;
+  return PAGEABLE;
+}
+
+constexpr int NS = 3;             // pipeline depth (slots/streams)
+constexpr int64_t CHUNK_PTS = 1 << 20;  // points per chunk (8 MiB per field)
+constexpr int NF = 9;             // w + u + 7 geometry fields per slot
+
+struct Stager {
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t st[NS] = {};
+  cudaEvent_t mats_ready = nullptr;
+  double* slots = nullptr;  // NS * NF * CHUNK_PTS doubles
+  double* mats = nullptr;   // 6 * 16 * 16 doubles
+};
+
+Stager g_stager[64];
+
+cudaError_t ensure(Stager& S) {
+  if (S.ready) return cudaSuccess;
+  cudaError_t e;
+  for (int s = 0; s < NS; ++s)
+    if ((e = cudaStreamCreateWithFlags(&S.st[s], cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&S.mats_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&S.slots, sizeof(double) * NS * NF * CHUNK_PTS)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&S.mats, sizeof(double) * 6 * 256)) != cudaSuccess) return e;
+  S.ready = true;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int mode) {
+  if (lx < 2 || lx > 16) return set_status(AXHELM_EINVAL, "lx=%d outside [2, 16]", lx);
+  if (nel < 0) return set_status(AXHELM_EINVAL, "nelv=%lld is negative", (long long)nel);
+  if (nel == 0) return set_status(AXHELM_OK, "");
+  for (int q = 0; q < 15; ++q)
+    if (!ptrs[q]) return set_status(AXHELM_EINVAL, "argument %d is NULL", q);
+
+  Kind kind[15];
+  bool all_dev = true;
+  for (int q = 0; q < 15; ++q) {
+    kind[q] = classify(ptrs[q]);
+    all_dev &= kind[q] == DEV;
+  }
+  const int64_t L3 = (int64_t)lx * lx * lx;
+
+  if (all_dev) {  // plain device call: run on the legacy default stream, synchronously
+    AxPtrs A{const_cast<double*>(ptrs[0]), ptrs[1], ptrs[2], ptrs[3], ptrs[4], ptrs[5],
+             ptrs[6], ptrs[7], ptrs[8], ptrs[9], ptrs[10], ptrs[11], ptrs[12], ptrs[13],
+             ptrs[14]};
+    cudaError_t e = launch_ax(A, nel, lx, mode, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    return cuda_status(e, "__dace_ax_helm (device)");
+  }
+
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_status(AXHELM_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  Stager& S = g_stager[dev & 63];
+  std::lock_guard<std::mutex> lock(S.mu);
+  if ((e = ensure(S)) != cudaSuccess) return cuda_status(e, "__dace_ax_helm (staging setup)");
+
+  // the six [lx][lx] matrices: once per call
+  const double* mat[6];
+  const size_t mbytes = sizeof(double) * lx * lx;
+  for (int q = 0; q < 6; ++q) {
+    if (kind[2 + q] == DEV) {
+      mat[q] = ptrs[2 + q];
+    } else {
+      double* d = S.mats + q * 256;
+      if ((e = cudaMemcpyAsync(d, ptrs[2 + q], mbytes, cudaMemcpyHostToDevice, S.st[0])) != cudaSuccess)
+        return cuda_status(e, "__dace_ax_helm (matrices)");
+      mat[q] = d;
+    }
+  }
+  cudaEventRecord(S.mats_ready, S.st[0]);
+  for (int s = 1; s < NS; ++s) cudaStreamWaitEvent(S.st[s], S.mats_ready, 0);
+
+  // field indices in ptrs[]: 0 = w, 1 = u, 8..14 = h1, g11, g22, g33, g12, g13, g23
+  static const int fidx[NF] = {0, 1, 8, 9, 10, 11, 12, 13, 14};
+  const int64_t chunk_el = CHUNK_PTS / L3 > 0 ? CHUNK_PTS / L3 : 1;
+  for (int64_t e0 = 0, c = 0; e0 < nel; e0 += chunk_el, ++c) {
+    const int s = (int)(c % NS);
+    const int64_t ne = (nel - e0 < chunk_el) ? nel - e0 : chunk_el;
+    const int64_t off = e0 * L3;
+    const size_t bytes = sizeof(double) * ne * L3;
+    double* slot = S.slots + (size_t)s * NF * CHUNK_PTS;
+    const double* f[NF];
+    for (int q = 0; q < NF; ++q) {
+      const int a = fidx[q];
+      if (kind[a] == DEV) {
+        f[q] = ptrs[a] + off;
+      } else {
+        double* d = slot + (size_t)q * CHUNK_PTS;
+        if (q > 0 &&
+            (e = cudaMemcpyAsync(d, ptrs[a] + off, bytes, cudaMemcpyHostToDevice, S.st[s])) != cudaSuccess)
+          return cuda_status(e, "__dace_ax_helm (H2D)");
+        f[q] = d;
+      }
+    }
+    AxPtrs A{const_cast<double*>(f[0]), f[1], mat[0], mat[1], mat[2], mat[3], mat[4], mat[5],
+             f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
+    if ((e = launch_ax(A, ne, lx, mode, S.st[s])) != cudaSuccess)
+      return cuda_status(e, "__dace_ax_helm (kernel)");
+    if (kind[0] != DEV &&
+        (e = cudaMemcpyAsync(const_cast<double*>(ptrs[0]) + off, f[0], bytes, cudaMemcpyDeviceToHost,
+                             S.st[s])) != cudaSuccess)
+      return cuda_status(e, "__dace_ax_helm (D2H)");
+  }
+  for (int s = 0; s < NS; ++s)
+    if ((e = cudaStreamSynchronize(S.st[s])) != cudaSuccess) return cuda_status(e, "__dace_ax_helm (sync)");
+  return set_status(AXHELM_OK, "");
+}
+
+}  // namespace axb

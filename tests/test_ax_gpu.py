@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a ax_helm against the pinned oracle and the
+reference's own golden digests.  All calls go through the reference-facing
+operator API (load_kernel -> KernelFn) and hence the C ABI.
+
+Tolerances: strict mode is bit-exact (sha256 of the output bytes equals the
+reference's); fast mode is <= 1e-12 normwise (max|d| / max|want|), the
+reference's relaxed-fp bar (tests/test_codegen.py:180-187,
+cabi-harness/test/conformance.test.ts:82-98).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    if not t.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return t
+
+
+@pytest.fixture(scope="module")
+def kern():
+    from paper_2506_20994_b200 import load_kernel
+
+    return {"strict": load_kernel(mode="strict"), "fast": load_kernel(mode="fast")}
+
+
+@pytest.fixture(scope="module")
+def digests(golden_dir):
+    return json.loads((golden_dir / "ax_digests.json").read_text())
+
+
+def run_dev(torch, fn, arrays, nel, lx):
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
+    dev["wd"].fill_(np.nan)  # every output point must be written
+    fn(dev, nel, lx)
+    torch.cuda.synchronize()
+    return dev["wd"].cpu().numpy()
+
+
+def test_golden_cases_bit_exact(torch, kern, golden_dir):
+    with np.load(golden_dir / "ax_cases.npz") as z:
+        tags = sorted({k.split("/")[0] for k in z.files})
+        for tag in tags:
+            arrays = {n: z[f"{tag}/{n}"] for n in o.ABI_ORDER if n != "wd"}
+            want = z[f"{tag}/expected_wd"]
+            nel, lx = want.shape[0], want.shape[1]
+            arrays["wd"] = np.zeros_like(want)
+            got = run_dev(torch, kern["strict"], arrays, nel, lx)
+            assert np.array_equal(got, want), tag
+            got = run_dev(torch, kern["fast"], arrays, nel, lx)
+            assert o.normwise_rel(got, want) <= FAST_TOL, tag
+
+
+@pytest.mark.parametrize("lx", range(2, 17))
+def test_bench_grid_strict_digest(torch, kern, digests, lx):
+    """lx 2..16 x nel {1,8,64} with bench._problem inputs: sha256(wd) equals
+    the digest of mdg.sem.ax_reference's output."""
+    for nel in (1, 8, 64):
+        rec = digests["bench"][f"{lx},{nel}"]
+        arrays = o.problem(lx, nel)
+        got = run_dev(torch, kern["strict"], arrays, nel, lx)
+        assert o.digest(got) == rec["wd"], (lx, nel)
+        assert float(got.sum()).hex() == rec["checksum"]  # bench.py:139-152 gate
+        fast = run_dev(torch, kern["fast"], arrays, nel, lx)
+        assert o.normwise_rel(fast, o.ax(arrays)) <= FAST_TOL, (lx, nel)
+
+
+def test_acceptance_grid_strict_digest(torch, kern, digests):
+    """test_acceptance.py:104-114 grid: lx 2..8 x nel {1,8,64} x 5 seeds."""
+    for key, rec in digests["acceptance"].items():
+        lx, nel, seed = map(int, key.split(","))
+        got = run_dev(torch, kern["strict"], o.problem(lx, nel, seed=seed), nel, lx)
+        assert o.digest(got) == rec["wd"], key
+
+
+def test_c1_oracle_config(torch, kern, digests):
+    """Config C1: lx=8, 512 elements, the oracle configuration."""
+    c1 = digests["C1"]
+    arrays = o.problem(8, 512)
+    got = run_dev(torch, kern["strict"], arrays, 512, 8)
+    assert o.digest(got) == c1["wd"]
+
+
+def test_six_matrix_slots_are_independent(torch, kern):
+    rng = np.random.default_rng(5)
+    for lx in (3, 8, 11):
+        arrays = o.problem(lx, 7)
+        for name in o.MATRICES:
+            arrays[name] = rng.standard_normal((lx, lx))
+        want = o.ax(arrays)
+        assert np.array_equal(run_dev(torch, kern["strict"], arrays, 7, lx), want)
+
+
+def test_host_pointer_path_chunked(torch, kern):
+    """__dace_ax_helm with HOST (numpy) buffers, enough elements for several
+    staging chunks, bit-exact against the C oracle."""
+    if o.c_oracle() is None:
+        pytest.skip("C oracle not built")
+    for lx, nel in ((8, 5000), (3, 40000), (12, 700)):
+        arrays = o.problem(lx, nel)
+        want = o.ax_c(arrays)
+        arrays["wd"] = np.full_like(want, np.nan)
+        kern["strict"](arrays, nel, lx)
+        assert np.array_equal(arrays["wd"], want), (lx, nel)
+
+
+def test_pinned_and_mixed_pointers(torch, kern):
+    lx, nel = 6, 3000
+    arrays = o.problem(lx, nel)
+    want = o.ax(arrays)
+    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in arrays.items()}
+    pinned["wd"].fill_(np.nan)
+    kern["strict"](pinned, nel, lx)
+    assert np.array_equal(pinned["wd"].numpy(), want)
+    # geometry on the device, u / w / matrices on the host
+    mixed = dict(pinned)
+    for k in ("h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d"):
+        mixed[k] = pinned[k].cuda()
+    mixed["wd"] = torch.full_like(pinned["wd"], float("nan"))
+    kern["strict"](mixed, nel, lx)
+    assert np.array_equal(mixed["wd"].numpy(), want)
+
+
+def test_reference_symbol_via_ctypes(torch):
+    """Bind __dace_ax_helm exactly as mdg.kernelrt does (kernelrt.py:84-106):
+    15 double* + int + int on host ndarrays."""
+    import ctypes
+
+    from paper_2506_20994_b200 import _lib
+
+    lib = ctypes.CDLL(str(_lib.lib_path()))
+    fn = lib.__dace_ax_helm
+    fn.restype = None
+    fn.argtypes = [ctypes.POINTER(ctypes.c_double)] * 15 + [ctypes.c_int, ctypes.c_int]
+    arrays = {k: np.ascontiguousarray(v) for k, v in o.problem(5, 64).items()}
+    ptrs = [arrays[n].ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for n in o.ABI_ORDER]
+    fn(*ptrs, 64, 5)
+    assert np.array_equal(arrays["wd"], o.ax(arrays))
+
+
+def test_edge_cases(torch, kern):
+    from paper_2506_20994_b200 import RangeError
+
+    arrays = o.problem(4, 1)
+    z = {k: v[:0] if v.ndim == 4 else v for k, v in arrays.items()}
+    kern["strict"](z, 0, 4)  # empty mesh: no-op
+    dz = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in z.items()}
+    kern["strict"](dz, 0, 4)
+    bad = {k: np.zeros((1, 17, 17, 17)) if v.ndim == 4 else np.zeros((17, 17)) for k, v in arrays.items()}
+    with pytest.raises(RangeError):
+        kern["strict"](bad, 1, 17)
+    # constants are annihilated (test_oracle.py:129-135)
+    arrays = o.problem(7, 9, seed=3)
+    arrays["ud"] = np.full_like(arrays["ud"], 3.75)
+    got = run_dev(torch, kern["fast"], arrays, 9, 7)
+    scale = max(float(np.abs(arrays[f]).max()) for f in o.FIELDS if f != "ud")
+    assert np.abs(got).max() <= 1e-11 * 3.75 * scale
+
+
+def test_full_size_sampled_elements_bit_exact(torch, kern):
+    """Config C2 (lx=8, 2^18 elements) generated on the device.  Elements are
+    independent, so the strict output of a random subset of elements (plus
+    the first and last, exercising 64-bit offsets) must equal the oracle
+    applied to just those elements; linearity and a checksum of checksums
+    cover the rest."""
+    from paper_2506_20994_b200 import gll_basis
+
+    lx, nel = 8, 1 << 18
+    g = torch.Generator(device="cuda").manual_seed(11)
+    shape = (nel, lx, lx, lx)
+    dev = {"wd": torch.empty(shape, dtype=torch.float64, device="cuda")}
+    dev["ud"] = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
+    for k in ("h1d", "g11d", "g22d", "g33d"):
+        dev[k] = torch.rand(shape, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    for k in ("g12d", "g13d", "g23d"):
+        dev[k] = torch.rand(shape, dtype=torch.float64, device="cuda", generator=g) * 0.2 - 0.1
+    a, b = gll_basis(lx).operator_matrices()
+    for n in ("dxd", "dyd", "dzd"):
+        dev[n] = torch.from_numpy(a).cuda()
+    for n in ("dxtd", "dytd", "dztd"):
+        dev[n] = torch.from_numpy(b).cuda()
+    kern["strict"](dev, nel, lx)
+    torch.cuda.synchronize()
+    idx = np.unique(np.concatenate([[0, nel - 1], np.random.default_rng(0).integers(0, nel, 300)]))
+    ti = torch.from_numpy(idx).cuda()
+    sub = {k: (v[ti].cpu().numpy() if v.dim() == 4 else v.cpu().numpy()) for k, v in dev.items()}
+    assert np.array_equal(sub["wd"], o.ax(sub))
+    # linearity of the fast path at full size: A(2u) = 2 A(u) exactly (power of 2 scaling)
+    w1 = dev["wd"].clone()
+    dev["ud"].mul_(2.0)
+    kern["strict"](dev, nel, lx)
+    torch.cuda.synchronize()
+    assert torch.equal(dev["wd"], 2.0 * w1)
