@@ -86,6 +86,14 @@ int axhelm_last_status(void);
 const char* axhelm_last_error(void);
 const char* axhelm_version(void);
 
+/* Roofline probe (diagnostics): lx = 8 only, same TMA ring and the same HBM
+ * traffic as the apply (8 fields read, wd written, wd = sum of the fields).
+ * Its time is the memory-side ceiling of the kernel design. */
+int axhelm_probe_stream(double* wd, const double* ud, const double* h1d,
+                        const double* g11d, const double* g22d, const double* g33d,
+                        const double* g12d, const double* g13d, const double* g23d,
+                        int64_t nel, void* stream);
+
 /* Algorithmic model: bytes = 72*nel*lx^3, flops =
  * nel*lx^3*(12*lx+18) (sem.py:367-375). */
 int64_t axhelm_bytes_model(int64_t nel, int lx);

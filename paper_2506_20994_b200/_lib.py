@@ -23,6 +23,7 @@ PROTOTYPES = {
     "__dace_ax_helm": (None, [_vp] * 15 + [ctypes.c_int, ctypes.c_int]),
     "axhelm_apply": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp]),
     "axhelm_apply_sync": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
+    "axhelm_probe_stream": (ctypes.c_int, [_vp] * 9 + [ctypes.c_int64, _vp]),
     "axhelm_set_mode": (ctypes.c_int, [ctypes.c_int]),
     "axhelm_get_mode": (ctypes.c_int, []),
     "axhelm_last_status": (ctypes.c_int, []),

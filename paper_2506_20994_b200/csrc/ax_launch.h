@@ -13,8 +13,12 @@ int set_status(int st, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 int default_mode();
 
-// enqueue one apply over device pointers (no validation)
-cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st);
+// enqueue one apply over device pointers (no validation).  hz / hzt / hx /
+// hxt: host copies of dzd / dztd / dxd / dxtd when the caller has them
+// (else looked up in / added to the pointer-keyed cache).
+cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
+                      const double* hz = nullptr, const double* hzt = nullptr,
+                      const double* hx = nullptr, const double* hxt = nullptr);
 
 // __dace_ax_helm body: classify the 15 pointers (device / pinned host /
 // pageable host) and run the apply synchronously, staging host data through

@@ -11,6 +11,9 @@
 
 #include "../../include/axhelm.h"
 #include "ax_kernels.cuh"
+#include "ax_tma.cuh"
+#include "ax_tma2.cuh"
+#include "ax_row.cuh"
 #include "ax_launch.h"
 
 #ifndef AXHELM_VERSION
@@ -61,18 +64,251 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int LX>
-static cudaError_t launch_lx(const AxPtrs& A, int64_t nel, int mode, cudaStream_t st) {
-  return mode == AXHELM_FAST ? launch_kwalk<LX, true>(A, nel, st)
-                             : launch_kwalk<LX, false>(A, nel, st);
+// Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
+// pf (v2, L2-prefetching k-walk), tma (v3, TMA ring), tma2 (v4: v3 +
+// constant-bank dz/dzt + k-split) or row (v5, row-per-thread; lx = 8);
+// default v4 where it applies (lx <= 8, 16-B aligned fields), else v2.  AXHELM_PF (1..3, lx = 8 only) sets
+// v2's prefetch distance in groups (default 1).
+static int g_variant = [] {
+  const char* v = getenv("AXHELM_KERNEL");
+  if (v && !strcmp(v, "kwalk")) return 1;
+  if (v && !strcmp(v, "pf")) return 2;
+  if (v && !strcmp(v, "tma")) return 3;
+  if (v && !strcmp(v, "row")) return 5;
+  return 4;
+}();
+static int g_pf = [] {
+  const char* v = getenv("AXHELM_PF");
+  int d = v ? atoi(v) : 1;
+  return (d >= 1 && d <= 3) ? d : 1;
+}();
+static int g_num_sms = 0;
+
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
 }
 
-cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st) {
+template <int LX, bool FAST>
+static cudaError_t launch_tma(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+  using C = TCfg<LX>;
+  static int blocks_per_sm = 0;  // benign race: idempotent
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_tma<LX, FAST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma<LX, FAST>, C::NT, C::SMEM);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm = b > 0 ? b : 1;
+  }
+  const int64_t groups = (nel + C::EPL - 1) / C::EPL;
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > groups) grid = groups;
+  ax_tma<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(A, nel);
+  return cudaGetLastError();
+}
+
+// ---- host copies of the t-direction matrices for the parameter block (v4)
+//
+// The kernel verifies the copy against the device arrays and falls back to
+// them (flagging *stale) if they differ, so a stale cache costs speed, never
+// correctness.
+struct MatEntry {
+  const double* dz = nullptr;
+  const double* dzt = nullptr;
+  int lx = 0;
+  uint64_t used = 0;
+  double z[256], zt[256];
+};
+static std::mutex g_mat_mu;
+static MatEntry g_mat[16];
+static uint64_t g_mat_clock = 0;
+static int* g_stale = nullptr;  // mapped pinned host flag
+
+static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, const double* hzt,
+                                 cudaStream_t st, double* z, double* zt, int** stale) {
+  const size_t n = (size_t)lx * lx;
+  std::lock_guard<std::mutex> lock(g_mat_mu);
+  if (!g_stale) {
+    cudaError_t e = cudaHostAlloc(&g_stale, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    *g_stale = 0;
+  }
+  *stale = g_stale;
+  if (hz && hzt) {
+    memcpy(z, hz, n * sizeof(double));
+    memcpy(zt, hzt, n * sizeof(double));
+    return cudaSuccess;
+  }
+  if (*(volatile int*)g_stale) {  // a kernel saw a changed matrix: drop every copy
+    for (auto& m : g_mat) m.dz = m.dzt = nullptr;
+    *(volatile int*)g_stale = 0;
+  }
+  MatEntry* hit = nullptr;
+  MatEntry* lru = &g_mat[0];
+  for (auto& m : g_mat) {
+    if (m.dz == A.dz && m.dzt == A.dzt && m.lx == lx) hit = &m;
+    if (m.used < lru->used) lru = &m;
+  }
+  if (!hit) {
+    hit = lru;
+    cudaError_t e = cudaMemcpyAsync(hit->z, A.dz, n * sizeof(double), cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hit->zt, A.dzt, n * sizeof(double), cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    hit->dz = A.dz;
+    hit->dzt = A.dzt;
+    hit->lx = lx;
+  }
+  hit->used = ++g_mat_clock;
+  memcpy(z, hit->z, n * sizeof(double));
+  memcpy(zt, hit->zt, n * sizeof(double));
+  return cudaSuccess;
+}
+
+static int g_nks8 = [] {
+  const char* v = getenv("AXHELM_NKS");
+  int d = v ? atoi(v) : 2;
+  return (d == 1 || d == 2 || d == 4) ? d : 2;
+}();
+
+template <int LX, bool FAST, int NKS>
+static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
+                               const double* hzt) {
+  using C = T2Cfg<LX, NKS>;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_tma2<LX, FAST, NKS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma2<LX, FAST, NKS>, C::NT, C::SMEM);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm = b > 0 ? b : 1;
+  }
+  TParams<LX> P;
+  P.A = A;
+  P.nel = nel;
+  double z[LX * LX], zt[LX * LX];
+  cudaError_t e = host_matrices(A, LX, hz, hzt, st, z, zt, &P.stale);
+  if (e != cudaSuccess) return e;
+  for (int l = 0; l < LX; ++l)
+    for (int k = 0; k < LX; ++k) {
+      P.zT[k * LX + l] = z[l * LX + k];
+      P.ztT[k * LX + l] = zt[l * LX + k];
+    }
+  const int64_t groups = (nel + C::EPL - 1) / C::EPL;
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > groups) grid = groups;
+  ax_tma2<LX, FAST, NKS><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <int LX, bool FAST>
+static cudaError_t launch_row(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hx,
+                              const double* hxt) {
+  using C = RCfg<LX>;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_row<LX, FAST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_row<LX, FAST>, C::NT, C::SMEM);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm = b > 0 ? b : 1;
+  }
+  RParams<LX> P;
+  P.A = A;
+  P.nel = nel;
+  // host copies of dxd / dxtd (same cache as v4's dzd / dztd: keyed by pointer)
+  AxPtrs Ax = A;
+  Ax.dz = A.dx;
+  Ax.dzt = A.dxt;
+  cudaError_t e = host_matrices(Ax, LX, hx, hxt, st, P.dx, P.dxt, &P.stale);
+  if (e != cudaSuccess) return e;
+  const int64_t groups = (nel + C::EPL - 1) / C::EPL;
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > groups) grid = groups;
+  ax_row<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+static bool aligned16(const AxPtrs& A) {
+  const void* f[9] = {A.w, A.u, A.h1, A.g11, A.g22, A.g33, A.g12, A.g13, A.g23};
+  for (const void* p : f)
+    if (((uintptr_t)p & 15u) != 0) return false;
+  return true;
+}
+
+template <int LX, bool FAST, int PF>
+static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+  using C = SCfg<LX>;
+  static int blocks_per_sm = 0;  // benign race: idempotent
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_kwalk_pf<LX, FAST, PF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_kwalk_pf<LX, FAST, PF>, C::NT,
+                                                      C::SMEM);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm = b > 0 ? b : 1;
+  }
+  const int64_t groups = (nel + C::EPB - 1) / C::EPB;
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > groups) grid = groups;
+  ax_kwalk_pf<LX, FAST, PF><<<(unsigned)grid, C::NT, C::SMEM, st>>>(A, nel);
+  return cudaGetLastError();
+}
+
+template <int LX, bool FAST>
+static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
+                                  const double* hzt, const double* hx, const double* hxt) {
+  if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
+  if constexpr (LX <= 8) {
+    if (g_variant == 3 && aligned16(A)) return launch_tma<LX, FAST>(A, nel, st);
+    if (g_variant == 5 && aligned16(A)) {
+      if constexpr (LX == 8) return launch_row<LX, FAST>(A, nel, st, hx, hxt);
+    }
+    if (g_variant >= 4 && aligned16(A)) {
+      if constexpr (LX == 8) {
+        if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
+        if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
+        return launch_tma2<LX, FAST, 2>(A, nel, st, hz, hzt);
+      } else {
+        return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
+      }
+    }
+  }
+  if constexpr (LX == 8) {
+    if (g_pf == 2) return launch_pf<LX, FAST, 2>(A, nel, st);
+    if (g_pf == 3) return launch_pf<LX, FAST, 3>(A, nel, st);
+  }
+  return launch_pf<LX, FAST, 1>(A, nel, st);
+}
+
+template <int LX>
+static cudaError_t launch_lx(const AxPtrs& A, int64_t nel, int mode, cudaStream_t st,
+                             const double* hz, const double* hzt, const double* hx,
+                             const double* hxt) {
+  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, hx, hxt)
+                             : launch_variant<LX, false>(A, nel, st, hz, hzt, hx, hxt);
+}
+
+cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
+                      const double* hz, const double* hzt, const double* hx, const double* hxt) {
   if (nel == 0) return cudaSuccess;
   switch (lx) {
 #define AXB_CASE(N) \
   case N:           \
-    return launch_lx<N>(A, nel, mode, st);
+    return launch_lx<N>(A, nel, mode, st, hz, hzt, hx, hxt);
     AXB_CASE(2) AXB_CASE(3) AXB_CASE(4) AXB_CASE(5) AXB_CASE(6) AXB_CASE(7)
     AXB_CASE(8) AXB_CASE(9) AXB_CASE(10) AXB_CASE(11) AXB_CASE(12)
     AXB_CASE(13) AXB_CASE(14) AXB_CASE(15) AXB_CASE(16)
@@ -153,6 +389,28 @@ int axhelm_get_mode(void) { return g_mode; }
 int axhelm_last_status(void) { return t_status; }
 const char* axhelm_last_error(void) { return t_msg; }
 const char* axhelm_version(void) { return "libaxhelm_sm100 " AXHELM_VERSION " (sm_100a, FP64)"; }
+
+int axhelm_probe_stream(double* wd, const double* ud, const double* h1d, const double* g11d,
+                        const double* g22d, const double* g33d, const double* g12d,
+                        const double* g13d, const double* g23d, int64_t nel, void* stream) {
+  // lx = 8 only: the roofline probe for the headline configuration
+  using C = TCfg<8>;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_stream_probe<8>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "axhelm_probe_stream");
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ax_stream_probe<8>, C::NT, C::SMEM);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  AxPtrs A{wd, ud, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+           h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > nel) grid = nel;
+  if (grid < 1) return set_status(AXHELM_OK, "");
+  ax_stream_probe<8><<<(unsigned)grid, C::NT, C::SMEM, (cudaStream_t)stream>>>(A, nel);
+  return cuda_status(cudaGetLastError(), "axhelm_probe_stream");
+}
 
 int64_t axhelm_bytes_model(int64_t nel, int lx) {
   return 72LL * nel * (int64_t)lx * lx * lx;

@@ -134,7 +134,11 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
     }
     AxPtrs A{const_cast<double*>(f[0]), f[1], mat[0], mat[1], mat[2], mat[3], mat[4], mat[5],
              f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
-    if ((e = launch_ax(A, ne, lx, mode, S.st[s])) != cudaSuccess)
+    const double* hz = kind[4] != DEV ? ptrs[4] : nullptr;   // dzd
+    const double* hzt = kind[7] != DEV ? ptrs[7] : nullptr;  // dztd
+    const double* hx = kind[2] != DEV ? ptrs[2] : nullptr;   // dxd
+    const double* hxt = kind[5] != DEV ? ptrs[5] : nullptr;  // dxtd
+    if ((e = launch_ax(A, ne, lx, mode, S.st[s], hz, hzt, hx, hxt)) != cudaSuccess)
       return cuda_status(e, "__dace_ax_helm (kernel)");
     if (kind[0] != DEV &&
         (e = cudaMemcpyAsync(const_cast<double*>(ptrs[0]) + off, f[0], bytes, cudaMemcpyDeviceToHost,

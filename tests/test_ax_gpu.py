@@ -203,3 +203,25 @@ def test_full_size_sampled_elements_bit_exact(torch, kern):
     kern["strict"](dev, nel, lx)
     torch.cuda.synchronize()
     assert torch.equal(dev["wd"], 2.0 * w1)
+
+
+def test_matrix_changed_in_place_is_honoured(torch, kern):
+    """The library caches host copies of the t-direction matrices keyed by
+    device pointer; a matrix rewritten in place (same pointer, new values)
+    must still be the one applied (the kernel verifies its copy)."""
+    lx, nel = 8, 300
+    arrays = o.problem(lx, nel)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
+    kern["strict"](dev, nel, lx)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays))
+    rng = np.random.default_rng(8)
+    for name in ("dzd", "dztd", "dxd"):
+        new = rng.standard_normal((lx, lx))
+        arrays[name] = new
+        dev[name].copy_(torch.from_numpy(new))
+        for _ in range(2):  # first call detects the stale copy, second uses a fresh one
+            dev["wd"].fill_(np.nan)
+            kern["strict"](dev, nel, lx)
+            torch.cuda.synchronize()
+            assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays)), name
