@@ -14,6 +14,7 @@
 #include "ax_tma.cuh"
 #include "ax_tma2.cuh"
 #include "ax_row.cuh"
+#include "ax_dmma.cuh"
 #include "ax_launch.h"
 
 #ifndef AXHELM_VERSION
@@ -66,16 +67,19 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
 // pf (v2, L2-prefetching k-walk), tma (v3, TMA ring), tma2 (v4: v3 +
-// constant-bank dz/dzt + k-split) or row (v5, row-per-thread; lx = 8);
-// default v4 where it applies (lx <= 8, 16-B aligned fields), else v2.  AXHELM_PF (1..3, lx = 8 only) sets
-// v2's prefetch distance in groups (default 1).
+// constant-bank dz/dzt + k-split), row (v5, row-per-thread; lx = 8) or
+// dmma (v6, FP64 tensor cores; fast mode, lx = 8).  Default ("auto"): v6 for
+// fast lx = 8, v4 for every other lx <= 8 (16-B aligned fields), else v2.
+// AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
 static int g_variant = [] {
   const char* v = getenv("AXHELM_KERNEL");
   if (v && !strcmp(v, "kwalk")) return 1;
   if (v && !strcmp(v, "pf")) return 2;
   if (v && !strcmp(v, "tma")) return 3;
   if (v && !strcmp(v, "row")) return 5;
-  return 4;
+  if (v && !strcmp(v, "tma2")) return 4;
+  if (v && !strcmp(v, "dmma")) return 6;
+  return 0;  // auto
 }();
 static int g_pf = [] {
   const char* v = getenv("AXHELM_PF");
@@ -239,6 +243,24 @@ static cudaError_t launch_row(const AxPtrs& A, int64_t nel, cudaStream_t st, con
   return cudaGetLastError();
 }
 
+static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+  using C = DmCfg;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(ax_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_dmma8, C::NT, C::SMEM);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm = b > 0 ? b : 1;
+  }
+  int64_t grid = (int64_t)blocks_per_sm * num_sms();
+  if (grid > nel) grid = nel;
+  ax_dmma8<<<(unsigned)grid, C::NT, C::SMEM, st>>>(A, nel);
+  return cudaGetLastError();
+}
+
 static bool aligned16(const AxPtrs& A) {
   const void* f[9] = {A.w, A.u, A.h1, A.g11, A.g22, A.g33, A.g12, A.g13, A.g23};
   for (const void* p : f)
@@ -274,10 +296,13 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
   if constexpr (LX <= 8) {
     if (g_variant == 3 && aligned16(A)) return launch_tma<LX, FAST>(A, nel, st);
+    if ((g_variant == 6 || g_variant == 0) && FAST && aligned16(A)) {
+      if constexpr (LX == 8) return launch_dmma8(A, nel, st);
+    }
     if (g_variant == 5 && aligned16(A)) {
       if constexpr (LX == 8) return launch_row<LX, FAST>(A, nel, st, hx, hxt);
     }
-    if (g_variant >= 4 && aligned16(A)) {
+    if ((g_variant >= 4 || g_variant == 0) && aligned16(A)) {
       if constexpr (LX == 8) {
         if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
         if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
