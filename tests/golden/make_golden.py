@@ -21,6 +21,8 @@ time reads /root/reference; the fixtures are what travel.
                   gen-opt kernel (codegen + kernelrt, strict fp) — proves the
                   compiled reference path agrees bit-for-bit too
   mdgt_2x2.t      MDGT bytes written by mdg.tensorfile.write_tensor
+  dump_lx*_nel*/  `mdg run --dump` directories (15 tensors, sizes.txt,
+                  expected_wd.t) written by the reference CLI
   lx2_box_stiffness.npy  8x8 dense operator of one lx=2 unit box
                   (mdg.sem.dense_assemble; hand-derived in test_oracle.py:137-158)
 """
@@ -145,6 +147,21 @@ def main() -> None:
             fn(arrays, nel, lx)
             gd[f"{lx},{nel}"] = sha(arrays["wd"])
     (OUT / "genopt_digests.json").write_text(json.dumps(gd, indent=1))
+
+    # ---- an `mdg run --dump` directory made by the reference CLI itself
+    #      (cli.py:115-153), the cabi-harness conformance input format
+    import subprocess
+    import tempfile
+
+    for lx, nel in ((4, 8), (8, 2)):
+        dump = OUT / f"dump_lx{lx}_nel{nel}"
+        with tempfile.TemporaryDirectory() as td:
+            env = dict(__import__("os").environ, PYTHONPATH=str(REF))
+            graph = Path(td) / "ax.mdg"
+            subprocess.run([sys.executable, "-m", "mdg", "build", "--lx", str(lx), "-o", str(graph)],
+                           check=True, env=env, capture_output=True)
+            subprocess.run([sys.executable, "-m", "mdg", "run", "-i", str(graph), "--nel", str(nel),
+                            "--seed", "1", "--dump", str(dump)], check=True, env=env, capture_output=True)
 
     # ---- MDGT bytes and the lx=2 stiffness
     tensorfile.write_tensor(OUT / "mdgt_2x2.t", np.array([[1.0, 2.0], [3.0, -0.5]]))
