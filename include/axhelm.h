@@ -94,6 +94,36 @@ int axhelm_probe_stream(double* wd, const double* ud, const double* h1d,
                         const double* g12d, const double* g13d, const double* g23d,
                         int64_t nel, void* stream);
 
+/* ---- box mesh, device geometry store, gather-scatter (DSSUM) -----------
+ * No reference counterpart (SPEC.md:14 scopes them out of the reference;
+ * PAPER.md:123 names gather-scatter as Neko's second ingredient).  All
+ * pointers are device pointers; every call is stream-ordered. */
+
+/* Global node ids of a z-slab [ez0, ez0 + nel/(nx*ny)) of an nx*ny*nz brick
+ * of lx^3 elements (element order e = (ez*ny + ey)*nx + ex); gid of point
+ * (gx, gy, gz) = (gz*NY + gy)*NX + gx with NX = nx*(lx-1)+1. */
+int axhelm_box_gid(int64_t* gid, int nx, int ny, int lx, int64_t ez0, int64_t nel, void* stream);
+
+/* Geometric factors (h1 = 1, G = w_i w_j w_k det J J^-1 J^-T) of the same
+ * slab of a smoothly deformed brick, X = X0 + amp*sin sin sin. */
+int axhelm_box_geometry(double* h1d, double* g11d, double* g22d, double* g33d, double* g12d,
+                        double* g13d, double* g23d, const double* gll_points,
+                        const double* gll_weights, int nx, int ny, int nz, int lx, int64_t ez0,
+                        int64_t nel, double amp, void* stream);
+
+/* DSSUM over n shared global nodes in CSR form: copies of node q are
+ * w[idx[offs[q]] .. idx[offs[q+1]-1]] in ascending order; each gets the sum
+ * (from 0.0, in that order).  idx_bytes = 4 (int32) or 8 (int64). */
+int axhelm_gs_sum(double* w, const int64_t* offs, const void* idx, int idx_bytes, int64_t n,
+                  void* stream);
+
+/* Interface-plane steps of the multi-GPU DSSUM: PARTIAL buf[slot[q]] = sum
+ * of own copies; FINISH continues from buf[slot[q]] with own copies, writes
+ * the sum to the copies and to buf; WRITE copies buf[slot[q]] to own copies. */
+enum axhelm_gs_op { AXHELM_GS_PARTIAL = 0, AXHELM_GS_FINISH = 1, AXHELM_GS_WRITE = 2 };
+int axhelm_gs_plane(int op, double* w, const int64_t* offs, const void* idx, int idx_bytes,
+                    const int64_t* slot, int64_t n, double* buf, void* stream);
+
 /* Algorithmic model: bytes = 72*nel*lx^3, flops =
  * nel*lx^3*(12*lx+18) (sem.py:367-375). */
 int64_t axhelm_bytes_model(int64_t nel, int lx);

@@ -302,8 +302,9 @@ def box_mesh_gid(nx: int, ny: int, nz: int, lx: int) -> np.ndarray:
 
 
 def dssum(w: np.ndarray, gid: np.ndarray) -> np.ndarray:
-    """Direct stiffness summation: every local copy of a global node gets the
-    sum of all copies, accumulated from 0.0 in ascending flat local index.
+    """Direct stiffness summation: every local copy of a SHARED global node
+    (multiplicity > 1) gets the sum of all copies, accumulated from 0.0 in
+    ascending flat local index; unshared points are left untouched.
 
     The deterministic order is the contract the CUDA gather kernel follows,
     which is what makes the result bit-exact.  (np.add.at applies updates in
@@ -314,12 +315,17 @@ def dssum(w: np.ndarray, gid: np.ndarray) -> np.ndarray:
     nglob = int(g.max()) + 1 if g.size else 0
     acc = np.zeros(nglob)
     np.add.at(acc, g, flat)
-    return acc[g].reshape(w.shape)
+    cnt = np.bincount(g, minlength=nglob)
+    out = flat.copy()
+    shared = cnt[g] > 1
+    out[shared] = acc[g[shared]]
+    return out.reshape(w.shape)
 
 
 def multiplicity(gid: np.ndarray) -> np.ndarray:
     """Number of local copies of each point's global node (float64)."""
-    return dssum(np.ones(gid.shape), gid)
+    g = gid.reshape(-1)
+    return np.bincount(g)[g].astype(np.float64).reshape(gid.shape)
 
 
 def gs_boundary_mask(nx: int, ny: int, nz: int, lx: int) -> np.ndarray:
@@ -333,3 +339,44 @@ def gs_boundary_mask(nx: int, ny: int, nz: int, lx: int) -> np.ndarray:
     gz = gid // (NX * NY)
     on = (gx == 0) | (gx == NX - 1) | (gy == 0) | (gy == NY - 1) | (gz == 0) | (gz == NZ - 1)
     return np.where(on, 0.0, 1.0)
+
+
+def box_mesh_gid_slab(nx: int, ny: int, nz: int, lx: int, ez0: int, ez1: int) -> np.ndarray:
+    """box_mesh_gid restricted to the element layers [ez0, ez1)."""
+    g = box_mesh_gid(nx, ny, nz, lx)
+    return g[ez0 * nx * ny: ez1 * nx * ny]
+
+
+def box_deformed_geometry(nx: int, ny: int, nz: int, lx: int, amp: float,
+                          ez0: int = 0, ez1: int | None = None) -> dict[str, np.ndarray]:
+    """Geometric factors of the deformed brick (restates the device
+    generator's formulas, csrc/mesh_gs.cu box_geom_kernel; parity unpinned:
+    there is no reference mesh).  X = X0 + d (1,1,1), d = amp/c_min sin sin sin;
+    G = w_i w_j w_k det J J^-1 J^-T, h1 = 1."""
+    ez1 = nz if ez1 is None else ez1
+    x, w, _ = gll(lx)
+    ez, ey, ex = np.meshgrid(np.arange(ez0, ez1), np.arange(ny), np.arange(nx), indexing="ij")
+    ex, ey, ez = (a.reshape(-1, 1, 1, 1).astype(np.float64) for a in (ex, ey, ez))
+    X0 = ex + 0.5 * (x[None, None, None, :] + 1.0)
+    Y0 = ey + 0.5 * (x[None, None, :, None] + 1.0)
+    Z0 = ez + 0.5 * (x[None, :, None, None] + 1.0)
+    cx, cy, cz = 2 * np.pi / nx, 2 * np.pi / ny, 2 * np.pi / nz
+    cmin = min(cx, cy, cz)
+    sx, csx = np.sin(cx * X0), np.cos(cx * X0)
+    sy, csy = np.sin(cy * Y0), np.cos(cy * Y0)
+    sz, csz = np.sin(cz * Z0), np.cos(cz * Z0)
+    grad = [amp * (cx / cmin) * csx * sy * sz, amp * (cy / cmin) * sx * csy * sz,
+            amp * (cz / cmin) * sx * sy * csz]
+    shape = np.broadcast(X0, Y0, Z0).shape
+    J = np.empty(shape + (3, 3))
+    for a in range(3):
+        for b in range(3):
+            J[..., a, b] = 0.5 * ((1.0 if a == b else 0.0) + grad[b])
+    Jinv = np.linalg.inv(J)
+    det = np.linalg.det(J)
+    W = w[None, :, None, None] * w[None, None, :, None] * w[None, None, None, :]
+    G = np.einsum("...ba,...ca->...bc", Jinv, Jinv) * (W * det)[..., None, None]
+    c = np.ascontiguousarray
+    return {"h1d": np.ones(shape), "g11d": c(G[..., 0, 0]), "g22d": c(G[..., 1, 1]),
+            "g33d": c(G[..., 2, 2]), "g12d": c(G[..., 0, 1]), "g13d": c(G[..., 0, 2]),
+            "g23d": c(G[..., 1, 2])}

@@ -24,6 +24,13 @@ PROTOTYPES = {
     "axhelm_apply": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp]),
     "axhelm_apply_sync": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
     "axhelm_probe_stream": (ctypes.c_int, [_vp] * 9 + [ctypes.c_int64, _vp]),
+    "axhelm_box_gid": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, _vp]),
+    "axhelm_box_geometry": (ctypes.c_int, [_vp] * 9 + [ctypes.c_int] * 4 + [ctypes.c_int64, ctypes.c_int64,
+                                                                          ctypes.c_double, _vp]),
+    "axhelm_gs_sum": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp]),
+    "axhelm_gs_plane": (ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp, ctypes.c_int64,
+                                       _vp, _vp]),
     "axhelm_set_mode": (ctypes.c_int, [ctypes.c_int]),
     "axhelm_get_mode": (ctypes.c_int, []),
     "axhelm_last_status": (ctypes.c_int, []),

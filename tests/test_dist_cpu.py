@@ -1,0 +1,104 @@
+"""The multi-rank DSSUM protocol (dist.py) over torch.distributed gloo on
+CPU, world sizes 2 and 3: every slab's result must equal the oracle's
+single-domain DSSUM bit for bit (oracle.dssum, ascending-local-order sums)."""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as o
+
+HERE = Path(__file__).resolve().parent
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, nx, ny, nz, lx, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, str(HERE))
+        from npgs import NumpyGSOps
+        from paper_2506_20994_b200.dist import SlabDSSUM, TorchComm
+        from paper_2506_20994_b200.mesh import slab_range
+
+        ez0, ez1 = slab_range(nz, rank, world)
+        gid = o.box_mesh_gid_slab(nx, ny, nz, lx, ez0, ez1)
+        n1 = lx - 1
+        ops = NumpyGSOps(gid, (nx * n1 + 1) * (ny * n1 + 1), n1, ez0, ez1, rank, world)
+        rng = np.random.default_rng(7)
+        wglob = rng.standard_normal((nx * ny * nz, lx, lx, lx))
+        want = o.dssum(wglob, o.box_mesh_gid(nx, ny, nz, lx))[ez0 * nx * ny: ez1 * nx * ny]
+        w = torch.from_numpy(wglob[ez0 * nx * ny: ez1 * nx * ny].copy())
+        SlabDSSUM(ops, TorchComm(dist))(w)
+        q.put((rank, bool(np.array_equal(w.numpy(), want)),
+               o.digest(w.numpy()) == o.digest(want)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims", [(2, (3, 2, 4, 3)), (3, (2, 3, 5, 4)), (2, (2, 2, 2, 8))])
+def test_slab_dssum_gloo_bit_exact(world, dims):
+    nx, ny, nz, lx = dims
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, ny, nz, lx, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok and dig for _, ok, dig in res), res
+
+
+def test_slab_range_and_mesh_counts():
+    from paper_2506_20994_b200.mesh import slab_range
+
+    assert [slab_range(10, r, 3) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
+    with pytest.raises(Exception):
+        slab_range(2, 0, 3)
+    gid = o.box_mesh_gid(3, 2, 2, 4)
+    m = o.multiplicity(gid)
+    assert m[0, 1, 1, 1] == 1  # element-interior point
+    assert m.max() == 8  # a vertex shared by 8 elements
+    n1 = 3
+    assert np.unique(gid).size == (3 * n1 + 1) * (2 * n1 + 1) * (2 * n1 + 1)
+
+
+def test_loopback_protocol_numpy():
+    """The single-process loopback driver over 3 slabs equals the oracle."""
+    sys.path.insert(0, str(HERE))
+    from npgs import NumpyGSOps
+    from paper_2506_20994_b200.dist import SlabDSSUM, loopback_dssum
+    from paper_2506_20994_b200.mesh import slab_range
+
+    nx, ny, nz, lx, world = 2, 2, 6, 3, 3
+    rng = np.random.default_rng(3)
+    wglob = rng.standard_normal((nx * ny * nz, lx, lx, lx))
+    want = o.dssum(wglob, o.box_mesh_gid(nx, ny, nz, lx))
+    slabs, ws = [], []
+    for r in range(world):
+        ez0, ez1 = slab_range(nz, r, world)
+        ops = NumpyGSOps(o.box_mesh_gid_slab(nx, ny, nz, lx, ez0, ez1),
+                         (nx * (lx - 1) + 1) * (ny * (lx - 1) + 1), lx - 1, ez0, ez1, r, world)
+        slabs.append(SlabDSSUM(ops, rank=r, world=world))
+        ws.append(torch.from_numpy(wglob[ez0 * nx * ny: ez1 * nx * ny].copy()))
+    loopback_dssum(slabs, ws)
+    got = np.concatenate([w.numpy() for w in ws])
+    assert np.array_equal(got, want)
