@@ -124,6 +124,16 @@ enum axhelm_gs_op { AXHELM_GS_PARTIAL = 0, AXHELM_GS_FINISH = 1, AXHELM_GS_WRITE
 int axhelm_gs_plane(int op, double* w, const int64_t* offs, const void* idx, int idx_bytes,
                     const int64_t* slot, int64_t n, double* buf, void* stream);
 
+/* Structured DSSUM on a BoxMesh slab (element layers [ez0, ez1) of an
+ * nx*ny*nz brick; no index arrays).  op 0: every shared node of the slab
+ * except those on an exchanged interface plane (has_below: bottom plane
+ * shared with the rank below; has_above: top plane shared with the rank
+ * above); op 1 + AXHELM_GS_PARTIAL / _FINISH / _WRITE: the interface-plane
+ * steps on buf[NX*NY] (PARTIAL, WRITE: top plane; FINISH: bottom plane).
+ * Same summation order as axhelm_gs_sum. */
+int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                  int has_below, int has_above, double* buf, void* stream);
+
 /* Algorithmic model: bytes = 72*nel*lx^3, flops =
  * nel*lx^3*(12*lx+18) (sem.py:367-375). */
 int64_t axhelm_bytes_model(int64_t nel, int lx);

@@ -31,6 +31,8 @@ PROTOTYPES = {
     "axhelm_gs_sum": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp]),
     "axhelm_gs_plane": (ctypes.c_int, [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp, ctypes.c_int64,
                                        _vp, _vp]),
+    "axhelm_gs_box": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp]),
     "axhelm_set_mode": (ctypes.c_int, [ctypes.c_int]),
     "axhelm_get_mode": (ctypes.c_int, []),
     "axhelm_last_status": (ctypes.c_int, []),

@@ -234,3 +234,193 @@ int axhelm_gs_plane(int op, double* w, const int64_t* offs, const void* idx, int
 }
 
 }  // extern "C"
+
+// ===================================================================
+// Structured DSSUM for BoxMesh slabs: the copies of a global node are found
+// arithmetically (no index arrays: the CSR path's ~4.3 B/point of offsets
+// and indices disappear; only the shared copies of w move).  One thread per
+// global node of the slab's node planes [gz_lo, gz_hi] (x fastest); copies
+// are visited in ascending (ez, ey, ex) = ascending local index, so the sum
+// order equals the CSR path's and the oracle's.
+// ===================================================================
+namespace axb {
+
+struct BoxGS {
+  int nx, ny, lx;
+  int64_t ez0, ez1;  // slab element layers
+  int64_t NX, NY;
+};
+
+// element range of global node coordinate g along an axis with ne elements
+__device__ __forceinline__ void node_elems(int64_t g, int n1, int64_t lo, int64_t hi, int64_t& e0,
+                                           int64_t& e1) {
+  // elements e with e*n1 <= g <= (e+1)*n1 (inclusive range), clipped to [lo, hi)
+  e0 = (g % n1 == 0) ? g / n1 - 1 : g / n1;
+  e1 = g / n1;
+  if (e0 < lo) e0 = lo;
+  if (e1 > hi - 1) e1 = hi - 1;
+}
+
+// Walks the copies of node (gx, gy, gz) in ascending local order: OP 0 sums
+// and writes back (skipping unshared nodes), 1 = PARTIAL (sum -> buf),
+// 2 = FINISH (continue from buf, write back, sum -> buf), 3 = WRITE (buf -> copies).
+template <int LX, int OP>
+__device__ __forceinline__ void gs_box_node(double* __restrict__ w, const BoxGS& M, int gx, int gy,
+                                            int gz, double* __restrict__ buf) {
+  constexpr int n1 = LX - 1;
+  constexpr int L3 = LX * LX * LX;
+  // each axis contributes one or two elements (a node on an element face)
+  const int x0 = max((gx % n1 == 0) ? gx / n1 - 1 : gx / n1, 0), x1 = min(gx / n1, M.nx - 1);
+  const int y0 = max((gy % n1 == 0) ? gy / n1 - 1 : gy / n1, 0), y1 = min(gy / n1, M.ny - 1);
+  const int z0 = max((gz % n1 == 0) ? gz / n1 - 1 : gz / n1, (int)M.ez0);
+  const int z1 = min(gz / n1, (int)M.ez1 - 1);
+  const int cx = x1 - x0 + 1, cy = y1 - y0 + 1, cz = z1 - z0 + 1;  // 1 or 2 each
+  if (OP == 0 && cx * cy * cz < 2) return;
+  const int64_t slot = (int64_t)gy * M.NX + gx;
+  // flat offsets of the (up to 8) copies, ascending (ez, ey, ex) = ascending local index
+  int64_t off[8];
+  bool ok[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+    ok[c] = dz < cz && dy < cy && dx < cx;
+    const int ez = z0 + dz, ey = y0 + dy, ex = x0 + dx;
+    const int64_t e = ((int64_t)(ez - M.ez0) * M.ny + ey) * M.nx + ex;
+    const int p = ((gz - ez * n1) * LX + (gy - ey * n1)) * LX + (gx - ex * n1);
+    off[c] = e * L3 + p;
+  }
+  double s = (OP == 2 || OP == 3) ? buf[slot] : 0.0;
+  if (OP != 3) {
+    double v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = ok[c] ? w[off[c]] : 0.0;  // independent loads
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (ok[c]) s = __dadd_rn(s, v[c]);
+  }
+  if (OP == 1) {
+    buf[slot] = s;
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (ok[c]) w[off[c]] = s;
+  if (OP == 2) buf[slot] = s;
+}
+
+// Interface-plane steps: one thread per node of plane gz (x fastest).
+template <int LX, int OP>
+__global__ void gs_box_plane_kernel(double* __restrict__ w, const BoxGS M, int gz,
+                                    double* __restrict__ buf) {
+  const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gx >= M.NX) return;
+  gs_box_node<LX, OP>(w, M, gx, blockIdx.y, gz, buf);
+}
+
+// Local DSSUM, enumerating only (potentially) shared nodes, densely:
+//  CLS 0: node planes on element faces (gz % n1 == 0): every (gx, gy)
+//  CLS 1: the other planes, rows on y faces (gy % n1 == 0): every gx
+//  CLS 2: the other planes and rows: x-face nodes only (gx = fx * n1)
+// z-plane sets are [zlo, zhi] (inclusive) of node planes owned locally.
+template <int LX, int CLS>
+__global__ void gs_box_local_kernel(double* __restrict__ w, const BoxGS M, int zlo, int zhi, int qlo) {
+  constexpr int n1 = LX - 1;
+  int gz, gy, gx;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (CLS == 0) {
+    gz = ((zlo + n1 - 1) / n1 + (int)blockIdx.z) * n1;  // face planes in [zlo, zhi]
+    gy = blockIdx.y;
+    gx = t;
+    if (gx >= M.NX) return;
+  } else {
+    // the q-th non-face node plane overall is (q/(n1-1))*n1 + 1 + q%(n1-1)
+    const int q = qlo + (int)blockIdx.z;
+    gz = (q / (n1 - 1)) * n1 + 1 + q % (n1 - 1);
+    if (CLS == 1) {
+      gy = (int)blockIdx.y * n1;
+      gx = t;
+      if (gx >= M.NX) return;
+    } else {
+      const int r = blockIdx.y;  // non-face row index
+      gy = (r / (n1 - 1)) * n1 + 1 + r % (n1 - 1);
+      gx = (t + 1) * n1;  // interior x faces fx = 1 .. nx-1
+      if (t >= M.nx - 1) return;
+    }
+  }
+  if (gz > zhi) return;
+  gs_box_node<LX, 0>(w, M, gx, gy, gz, nullptr);
+}
+
+template <int LX>
+static cudaError_t gs_box_launch(int op, double* w, const BoxGS& M, int has_below, int has_above,
+                                 double* buf, cudaStream_t st) {
+  constexpr int n1 = LX - 1;
+  const dim3 blk(128);
+  const unsigned gxb = (unsigned)((M.NX + 127) / 128);
+  switch (op) {
+    case 0: {
+      const int lo = (int)(M.ez0 * n1 + (has_below ? 1 : 0));
+      const int hi = (int)(M.ez1 * n1 - (has_above ? 1 : 0));
+      if (hi < lo) break;
+      // face planes in [lo, hi]
+      const int f0 = (lo + n1 - 1) / n1, f1 = hi / n1;
+      if (f1 >= f0)
+        gs_box_local_kernel<LX, 0><<<dim3(gxb, (unsigned)M.NY, (unsigned)(f1 - f0 + 1)), blk, 0, st>>>(
+            w, M, lo, hi, 0);
+      if (n1 > 1) {
+        // non-face planes in [lo, hi]
+        const int nnf = (hi - lo + 1) - (f1 >= f0 ? f1 - f0 + 1 : 0);
+        const int lo2 = (lo % n1 == 0) ? lo + 1 : lo;
+        const int qlo = (lo2 / n1) * (n1 - 1) + (lo2 % n1 - 1);
+        if (nnf > 0) {
+          gs_box_local_kernel<LX, 1><<<dim3(gxb, (unsigned)(M.ny + 1), (unsigned)nnf), blk, 0, st>>>(
+              w, M, lo, hi, qlo);
+          if (M.nx > 1)
+            gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
+                                              (unsigned)(M.ny * (n1 - 1)), (unsigned)nnf),
+                                         blk, 0, st>>>(w, M, lo, hi, qlo);
+        }
+      }
+      break;
+    }
+    case 1 + AXHELM_GS_PARTIAL:
+      gs_box_plane_kernel<LX, 1><<<dim3(gxb, (unsigned)M.NY, 1), blk, 0, st>>>(w, M, (int)(M.ez1 * n1), buf);
+      break;
+    case 1 + AXHELM_GS_FINISH:
+      gs_box_plane_kernel<LX, 2><<<dim3(gxb, (unsigned)M.NY, 1), blk, 0, st>>>(w, M, (int)(M.ez0 * n1), buf);
+      break;
+    case 1 + AXHELM_GS_WRITE:
+      gs_box_plane_kernel<LX, 3><<<dim3(gxb, (unsigned)M.NY, 1), blk, 0, st>>>(w, M, (int)(M.ez1 * n1), buf);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace axb
+
+extern "C" int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                             int has_below, int has_above, double* buf, void* stream) {
+  if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez1 <= ez0 || ez0 < 0)
+    return set_status(AXHELM_EINVAL, "axhelm_gs_box: bad sizes");
+  if (op < 0 || op > 3) return set_status(AXHELM_EINVAL, "axhelm_gs_box: unknown op %d", op);
+  const int n1 = lx - 1;
+  BoxGS M{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1};
+  if (M.NY > 65535 || ez1 * n1 >= (int64_t)1 << 31 || (op == 0 && (ez1 - ez0) * n1 + 1 > 65535))
+    return set_status(AXHELM_EINVAL, "axhelm_gs_box: mesh too large for the structured path");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (lx) {
+#define AXB_GSB(N) \
+  case N:          \
+    e = gs_box_launch<N>(op, w, M, has_below, has_above, buf, st); \
+    break;
+    AXB_GSB(2) AXB_GSB(3) AXB_GSB(4) AXB_GSB(5) AXB_GSB(6) AXB_GSB(7) AXB_GSB(8) AXB_GSB(9)
+    AXB_GSB(10) AXB_GSB(11) AXB_GSB(12) AXB_GSB(13) AXB_GSB(14) AXB_GSB(15) AXB_GSB(16)
+#undef AXB_GSB
+    default:
+      e = cudaErrorInvalidValue;
+  }
+  return cuda_status(e, "axhelm_gs_box");
+}

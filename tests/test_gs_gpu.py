@@ -44,30 +44,38 @@ def test_geometry_matches_oracle_and_is_spd(torch):
     assert det.min() > 0 and g["g11d"].min() > 0
 
 
-@pytest.mark.parametrize("dims", [(3, 2, 2, 2), (2, 3, 2, 3), (3, 3, 3, 5), (4, 2, 3, 8), (2, 2, 2, 12)])
-def test_dssum_single_slab_bit_exact(torch, dims):
-    from paper_2506_20994_b200.gs import GatherScatter
+GS_KINDS = ("csr", "box")
+
+
+def make_gs(kind, m, torch):
+    from paper_2506_20994_b200.gs import BoxGatherScatter, GatherScatter
+
+    return GatherScatter(m, torch, "cuda") if kind == "csr" else BoxGatherScatter(m, torch, "cuda")
+
+
+@pytest.mark.parametrize("kind", GS_KINDS)
+@pytest.mark.parametrize("dims", [(3, 2, 2, 2), (2, 3, 2, 3), (3, 3, 3, 5), (4, 2, 3, 8), (2, 2, 2, 12), (1, 1, 1, 4)])
+def test_dssum_single_slab_bit_exact(torch, dims, kind):
     from paper_2506_20994_b200.mesh import BoxMesh
     from paper_2506_20994_b200.dist import SlabDSSUM
 
     nx, ny, nz, lx = dims
     m = BoxMesh(nx, ny, nz, lx)
-    gs = GatherScatter(m, torch, "cuda")
     w = np.random.default_rng(sum(dims)).standard_normal(m.shape)
     want = o.dssum(w, o.box_mesh_gid(nx, ny, nz, lx))
     wd = torch.from_numpy(w).cuda()
-    SlabDSSUM(gs)(wd)
+    SlabDSSUM(make_gs(kind, m, torch))(wd)
     torch.cuda.synchronize()
     assert o.digest(wd.cpu().numpy()) == o.digest(want)
 
 
-@pytest.mark.parametrize("world,dims", [(2, (3, 2, 4, 4)), (3, (2, 3, 6, 8)), (4, (2, 2, 4, 3))])
-def test_dssum_loopback_slabs_bit_exact(torch, world, dims):
+@pytest.mark.parametrize("kind", GS_KINDS)
+@pytest.mark.parametrize("world,dims", [(2, (3, 2, 4, 4)), (3, (2, 3, 6, 8)), (4, (2, 2, 4, 3)), (3, (1, 2, 3, 5))])
+def test_dssum_loopback_slabs_bit_exact(torch, world, dims, kind):
     """Several slabs of one mesh on one GPU, interface planes exchanged by
     device copies: the multi-GPU kernels and protocol, bit-exact vs the
     single-domain oracle."""
     from paper_2506_20994_b200.dist import SlabDSSUM, loopback_dssum
-    from paper_2506_20994_b200.gs import GatherScatter
     from paper_2506_20994_b200.mesh import BoxMesh
 
     nx, ny, nz, lx = dims
@@ -76,7 +84,7 @@ def test_dssum_loopback_slabs_bit_exact(torch, world, dims):
     slabs, ws = [], []
     for r in range(world):
         m = BoxMesh(nx, ny, nz, lx, r, world)
-        slabs.append(SlabDSSUM(GatherScatter(m, torch, "cuda"), rank=r, world=world))
+        slabs.append(SlabDSSUM(make_gs(kind, m, torch), rank=r, world=world))
         ws.append(torch.from_numpy(w[m.ez0 * nx * ny: m.ez1 * nx * ny].copy()).cuda())
     loopback_dssum(slabs, ws)
     torch.cuda.synchronize()
@@ -89,14 +97,14 @@ def test_assembled_operator_annihilates_constants_on_the_mesh(torch):
     constant field vanishes to rounding."""
     from paper_2506_20994_b200 import load_kernel
     from paper_2506_20994_b200.dist import SlabDSSUM
-    from paper_2506_20994_b200.gs import GatherScatter
+    from paper_2506_20994_b200.gs import BoxGatherScatter
     from paper_2506_20994_b200.mesh import BoxMesh
 
     m = BoxMesh(4, 4, 4, 8)
     arr = {**m.geometry(torch, "cuda"), **m.matrices(torch, "cuda")}
     arr["ud"] = torch.full(m.shape, 2.5, dtype=torch.float64, device="cuda")
     arr["wd"] = torch.empty_like(arr["ud"])
-    dss = SlabDSSUM(GatherScatter(m, torch, "cuda"))
+    dss = SlabDSSUM(BoxGatherScatter(m, torch, "cuda"))
     for mode in ("strict", "fast"):
         load_kernel(mode=mode)(arr, m.nel, m.lx)
         dss(arr["wd"])
