@@ -134,6 +134,31 @@ int axhelm_gs_plane(int op, double* w, const int64_t* offs, const void* idx, int
 int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
                   int has_below, int has_above, double* buf, void* stream);
 
+/* ---- Jacobi-PCG building blocks (no reference) --------
+ * Deterministic reductions: `partial` holds axhelm_reduce_blocks(n) * 2
+ * doubles of scratch; results land in DEVICE memory (`out`), and alpha /
+ * beta are read from device memory, so an iteration needs no host sync. */
+int axhelm_reduce_blocks(int64_t n);
+/* out[0] = sum a*b (times wt if non-NULL) */
+int axhelm_dot(const double* a, const double* b, const double* wt, int64_t n, double* partial,
+               double* out, void* stream);
+/* r = mask*f, p = dinv*r, x = 0; out = {sum minv r dinv r, sum minv r r} */
+int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* minv,
+                   double* r, double* p, double* x, int64_t n, double* partial, double* out,
+                   void* stream);
+/* alpha = sc[0]/sc[1]; x += alpha p; r -= alpha mask w; out = {rz, rr} */
+int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* mask,
+                     const double* dinv, const double* minv, const double* sc, int64_t n,
+                     double* partial, double* out, void* stream);
+/* p = dinv r + (sc_new[0]/sc_old[0]) p */
+int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const double* sc_new,
+                      const double* sc_old, int64_t n, void* stream);
+/* element-local diagonal of A (the Jacobi preconditioner before DSSUM) */
+int axhelm_diag(double* diag, const double* dxd, const double* dyd, const double* dzd,
+                const double* dxtd, const double* dytd, const double* dztd, const double* h1d,
+                const double* g11d, const double* g22d, const double* g33d, const double* g12d,
+                const double* g13d, const double* g23d, int64_t nel, int lx, void* stream);
+
 /* Algorithmic model: bytes = 72*nel*lx^3, flops =
  * nel*lx^3*(12*lx+18) (sem.py:367-375). */
 int64_t axhelm_bytes_model(int64_t nel, int lx);

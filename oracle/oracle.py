@@ -380,3 +380,53 @@ def box_deformed_geometry(nx: int, ny: int, nz: int, lx: int, amp: float,
     return {"h1d": np.ones(shape), "g11d": c(G[..., 0, 0]), "g22d": c(G[..., 1, 1]),
             "g33d": c(G[..., 2, 2]), "g12d": c(G[..., 0, 1]), "g13d": c(G[..., 0, 2]),
             "g23d": c(G[..., 1, 2])}
+
+
+def local_diag(arrays: dict[str, np.ndarray]) -> np.ndarray:
+    """Diagonal of each element's A_e by applying ax() to unit vectors
+    (parity unpinned; restates sem.dense_assemble's column-by-column idea,
+    sem.py:340-364, per element)."""
+    u = arrays["ud"]
+    nel, lx = u.shape[0], u.shape[1]
+    n = lx ** 3
+    out = np.empty_like(u)
+    for e in range(nel):
+        sub = {k: (np.broadcast_to(v[e:e + 1], (n, lx, lx, lx)).copy() if v.ndim == 4 else v)
+               for k, v in arrays.items()}
+        sub["ud"] = np.eye(n).reshape(n, lx, lx, lx)
+        w = ax(sub).reshape(n, n)
+        out[e] = np.diag(w).reshape(lx, lx, lx)
+    return out
+
+
+def pcg(arrays: dict[str, np.ndarray], gid: np.ndarray, mask: np.ndarray, f: np.ndarray,
+        iters: int):
+    """Jacobi-PCG for mask.Q Q^T A x = mask.f from x = 0, the algorithm of
+    paper_2506_20994_b200/cg.py restated in NumPy (parity unpinned: the
+    reference has no solver).  Returns (x, rr_history)."""
+    mult = multiplicity(gid)
+    minv = 1.0 / mult
+    diag = dssum(local_diag(arrays), gid)
+    dinv = np.where(mask > 0, 1.0 / diag, 0.0)
+
+    def A(p):
+        a = dict(arrays)
+        a["ud"] = p
+        return dssum(ax(a), gid)
+
+    x = np.zeros_like(f)
+    r = mask * f
+    p = dinv * r
+    rz = float(np.sum(minv * r * dinv * r))
+    hist = [float(np.sum(minv * r * r))]
+    for _ in range(iters):
+        w = A(p)
+        pw = float(np.sum(minv * p * w))
+        alpha = rz / pw
+        x = x + alpha * p
+        r = r - alpha * mask * w
+        rz_new = float(np.sum(minv * r * dinv * r))
+        hist.append(float(np.sum(minv * r * r)))
+        p = dinv * r + (rz_new / rz) * p
+        rz = rz_new
+    return x, np.array(hist)

@@ -1,0 +1,112 @@
+"""Jacobi-preconditioned conjugate gradients for the assembled SEM Poisson
+problem  Q Q^T A x = f,  x = 0 on the brick's outer boundary (SURVEY §8f,
+config C5: 100 iterations, lx=8, 2^21 elements).
+
+No reference implementation (SPEC.md:14 — the Poisson solve is a non-goal);
+the weak form is PAPER.md:126-130 and the operator is HelmholtzOperator
+(ax_helm + DSSUM + interface exchange).  Vectors are local-point fields
+[nel][lx][lx][lx], continuous across elements (equal on all copies of a
+node); global inner products weight each copy by 1/multiplicity so every
+node counts once:  <a, b> = sum_p a_p b_p / mult_p  (all-reduced over ranks).
+
+One iteration (no host synchronisation; scalars live in device memory):
+  w  = mask . Q Q^T A p                     (operator.apply)
+  pw = <p, w>                               (axhelm_dot + all-reduce)
+  x += a p ; r -= a mask w ; rz', rr        (axhelm_cg_update + all-reduce)
+  p  = dinv r + (rz'/rz) p                  (axhelm_cg_pupdate)
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .errors import DeviceError
+from .operator import HelmholtzOperator
+
+
+class JacobiPCG:
+    def __init__(self, op: HelmholtzOperator):
+        self.op = op
+        m = op.mesh
+        torch = op.torch
+        dev = op.device
+        self.torch = torch
+        self.lib = _lib.load()
+        self.n = m.nel * m.lx ** 3
+        f64 = dict(dtype=torch.float64, device=dev)
+        # Dirichlet mask on the brick's outer boundary
+        gid = m.gid(torch, dev)
+        gx = gid % m.NX
+        gy = (gid // m.NX) % m.NY
+        gz = gid // m.plane
+        nz_nodes = m.nz * m.n1 + 1
+        on = (gx == 0) | (gx == m.NX - 1) | (gy == 0) | (gy == m.NY - 1) | (gz == 0) | (gz == nz_nodes - 1)
+        self.mask = (~on).to(torch.float64)
+        del gid, gx, gy, gz, on
+        # multiplicity (DSSUM of ones, across ranks) and the Jacobi diagonal
+        mult = torch.ones(m.shape, **f64)
+        op.dssum(mult)
+        self.minv = (1.0 / mult).contiguous()
+        del mult
+        diag = torch.empty(m.shape, **f64)
+        g = op.geom
+        mt = op.mats
+        rc = self.lib.axhelm_diag(diag.data_ptr(), *[mt[k].data_ptr() for k in
+                                                     ("dxd", "dyd", "dzd", "dxtd", "dytd", "dztd")],
+                                  *[g[k].data_ptr() for k in ("h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d")],
+                                  m.nel, m.lx, self._s())
+        if rc:
+            raise DeviceError(_lib.last_error(self.lib))
+        op.dssum(diag)
+        self.dinv = torch.where(self.mask > 0, 1.0 / diag, torch.zeros_like(diag)).contiguous()
+        del diag
+        self.x = torch.zeros(m.shape, **f64)
+        self.r = torch.empty(m.shape, **f64)
+        self.p = torch.empty(m.shape, **f64)
+        self.w = torch.empty(m.shape, **f64)
+        nb = self.lib.axhelm_reduce_blocks(self.n)
+        self.partial = torch.empty(2 * nb, **f64)
+
+    def _s(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.op.device).cuda_stream)
+
+    def _check(self, rc):
+        if rc:
+            raise DeviceError(_lib.last_error(self.lib))
+
+    def _allreduce(self, t):
+        if self.op.comm is not None and self.op.mesh.world > 1:
+            self.op.comm.allreduce_sum(t)
+
+    def solve(self, f, iters: int = 100):
+        """Run `iters` PCG iterations from x = 0.  Returns (x, rr_history)
+        where rr_history[i] = <r_i, r_i> (device tensor, i = 0..iters)."""
+        torch = self.torch
+        dev = self.op.device
+        n = self.n
+        # per-iteration scalar slots: sc[i] = (rz_i, rr_i), pw[i]
+        sc = torch.zeros(iters + 1, 2, dtype=torch.float64, device=dev)
+        pw = torch.zeros(iters, 1, dtype=torch.float64, device=dev)
+        s = self._s()
+        x, r, p, w = self.x, self.r, self.p, self.w
+        P = self.partial.data_ptr()
+        self._check(self.lib.axhelm_cg_init(f.data_ptr(), self.mask.data_ptr(), self.dinv.data_ptr(),
+                                            self.minv.data_ptr(), r.data_ptr(), p.data_ptr(),
+                                            x.data_ptr(), n, P, sc[0].data_ptr(), s))
+        self._allreduce(sc[0])
+        for it in range(iters):
+            self.op.apply(p, w)
+            self._check(self.lib.axhelm_dot(p.data_ptr(), w.data_ptr(), self.minv.data_ptr(), n, P,
+                                            pw[it].data_ptr(), s))
+            self._allreduce(pw[it])
+            # update reads (rz, pw) as a 2-vector: stage them contiguously
+            a = torch.stack((sc[it, 0], pw[it, 0]))
+            self._check(self.lib.axhelm_cg_update(x.data_ptr(), r.data_ptr(), p.data_ptr(), w.data_ptr(),
+                                                  self.mask.data_ptr(), self.dinv.data_ptr(),
+                                                  self.minv.data_ptr(), a.data_ptr(), n, P,
+                                                  sc[it + 1].data_ptr(), s))
+            self._allreduce(sc[it + 1])
+            self._check(self.lib.axhelm_cg_pupdate(p.data_ptr(), r.data_ptr(), self.dinv.data_ptr(),
+                                                   sc[it + 1].data_ptr(), sc[it].data_ptr(), n, s))
+        return x, sc[:, 1]

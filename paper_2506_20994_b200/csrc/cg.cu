@@ -1,0 +1,204 @@
+// Jacobi-preconditioned CG building blocks for the assembled SEM Poisson
+// operator (config C5).  No reference implementation:
+// the solve is a reference non-goal; the weak form is
+// PAPER.md:126-130.  Parity: oracle/oracle.py (NumPy PCG, same algorithm).
+//
+// Every kernel is a single fused pass over the local points; scalars (alpha,
+// beta) are read from DEVICE memory, so an iteration needs no host round
+// trip (graph-capturable; multi-GPU sums via NCCL all-reduce of the scalar
+// slots).  Reductions are deterministic: grid-stride partials per block in
+// a fixed order, then one block sums the partials in a fixed tree.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/axhelm.h"
+#include "ax_launch.h"
+
+namespace axb {
+
+constexpr int RT = 256;  // reduction block size
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = RT / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// partial[NQ*blockIdx.x + q] for q < NQ
+template <int NQ>
+__device__ __forceinline__ void write_partials(const double (&v)[NQ], double* partial) {
+  __shared__ double sh[RT];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double s = block_sum(v[q], sh);
+    if (threadIdx.x == 0) partial[NQ * blockIdx.x + q] = s;
+  }
+}
+
+// out[q] = sum_b partial[NQ*b + q]  (one block, fixed order)
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks, int nq,
+                                       double* __restrict__ out) {
+  __shared__ double sh[RT];
+  for (int q = 0; q < nq; ++q) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += RT) v += partial[nq * b + q];
+    const double s = block_sum(v, sh);
+    if (threadIdx.x == 0) out[q] = s;
+  }
+}
+
+// sum a*b (weights w if non-null)
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ wt, int64_t n, double* __restrict__ partial) {
+  double v[1] = {0.0};
+  for (int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x; p < n; p += (int64_t)gridDim.x * RT)
+    v[0] += wt ? wt[p] * a[p] * b[p] : a[p] * b[p];
+  write_partials<1>(v, partial);
+}
+
+// r = mask*f ; p = dinv*r ; partial: rz = sum minv r dinv r, rr = sum minv r r
+__global__ void cg_init_kernel(const double* __restrict__ f, const double* __restrict__ mask,
+                               const double* __restrict__ dinv, const double* __restrict__ minv,
+                               double* __restrict__ r, double* __restrict__ p,
+                               double* __restrict__ x, int64_t n, double* __restrict__ partial) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t q = (int64_t)blockIdx.x * RT + threadIdx.x; q < n; q += (int64_t)gridDim.x * RT) {
+    const double rr = mask[q] * f[q];
+    const double z = dinv[q] * rr;
+    r[q] = rr;
+    p[q] = z;
+    x[q] = 0.0;
+    v[0] += minv[q] * rr * z;
+    v[1] += minv[q] * rr * rr;
+  }
+  write_partials<2>(v, partial);
+}
+
+// alpha = sc[0] / sc[1] (rz / pw); x += alpha p; r -= alpha mask w;
+// partial: rz' = sum minv r dinv r, rr = sum minv r r
+__global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
+                                 const double* __restrict__ p, const double* __restrict__ w,
+                                 const double* __restrict__ mask, const double* __restrict__ dinv,
+                                 const double* __restrict__ minv, const double* __restrict__ sc,
+                                 int64_t n, double* __restrict__ partial) {
+  const double alpha = sc[0] / sc[1];
+  double v[2] = {0.0, 0.0};
+  for (int64_t q = (int64_t)blockIdx.x * RT + threadIdx.x; q < n; q += (int64_t)gridDim.x * RT) {
+    x[q] = fma(alpha, p[q], x[q]);
+    const double rr = fma(-alpha, mask[q] * w[q], r[q]);
+    r[q] = rr;
+    v[0] += minv[q] * rr * dinv[q] * rr;
+    v[1] += minv[q] * rr * rr;
+  }
+  write_partials<2>(v, partial);
+}
+
+// beta = sc_new[0] / sc_old[0]; p = dinv r + beta p
+__global__ void cg_pupdate_kernel(double* __restrict__ p, const double* __restrict__ r,
+                                  const double* __restrict__ dinv, const double* __restrict__ sc_new,
+                                  const double* __restrict__ sc_old, int64_t n) {
+  const double beta = sc_new[0] / sc_old[0];
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    p[q] = fma(beta, p[q], dinv[q] * r[q]);
+}
+
+// Local diagonal of A_e (closed form of ax_helm applied to unit vectors):
+//  sum_l dxt[l][i] dx[i][l] (h1 g11)(k,j,l) + sum_l dyt[l][j] dy[j][l] (h1 g22)(k,l,i)
+//  + sum_l dzt[l][k] dz[k][l] (h1 g33)(l,j,i) + h1(p) [ dxt[i][i] (g12 dy[j][j] + g13 dz[k][k])
+//  + dyt[j][j] (g12 dx[i][i] + g23 dz[k][k]) + dzt[k][k] (g13 dx[i][i] + g23 dy[j][j]) ](p)
+__global__ void diag_kernel(double* __restrict__ dg, const AxPtrs A, int lx, int64_t npts) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npts) return;
+  const int L2 = lx * lx, L3 = L2 * lx;
+  const int64_t e = q / L3;
+  const int p = (int)(q - e * L3);
+  const int k = p / L2, j = (p / lx) % lx, i = p % lx;
+  const int64_t b = e * L3;
+  double s = 0.0;
+  for (int l = 0; l < lx; ++l) {
+    const int64_t qx = b + (k * lx + j) * lx + l, qy = b + (k * lx + l) * lx + i, qz = b + (l * lx + j) * lx + i;
+    s += A.dxt[l * lx + i] * A.dx[i * lx + l] * A.h1[qx] * A.g11[qx];
+    s += A.dyt[l * lx + j] * A.dy[j * lx + l] * A.h1[qy] * A.g22[qy];
+    s += A.dzt[l * lx + k] * A.dz[k * lx + l] * A.h1[qz] * A.g33[qz];
+  }
+  const double dxi = A.dx[i * lx + i], dyj = A.dy[j * lx + j], dzk = A.dz[k * lx + k];
+  s += A.h1[q] * (A.dxt[i * lx + i] * (A.g12[q] * dyj + A.g13[q] * dzk) +
+                  A.dyt[j * lx + j] * (A.g12[q] * dxi + A.g23[q] * dzk) +
+                  A.dzt[k * lx + k] * (A.g13[q] * dxi + A.g23[q] * dyj));
+  dg[q] = s;
+}
+
+static int red_blocks(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t b = (n + RT - 1) / RT;
+  const int64_t cap = (int64_t)sms * 8;
+  return (int)(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+}  // namespace axb
+
+using namespace axb;
+
+extern "C" {
+
+int axhelm_reduce_blocks(int64_t n) { return red_blocks(n); }
+
+int axhelm_dot(const double* a, const double* b, const double* wt, int64_t n, double* partial,
+               double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = red_blocks(n);
+  dot_kernel<<<nb, RT, 0, st>>>(a, b, wt, n, partial);
+  reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
+  return cuda_status(cudaGetLastError(), "axhelm_dot");
+}
+
+int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* minv,
+                   double* r, double* p, double* x, int64_t n, double* partial, double* out,
+                   void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = red_blocks(n);
+  cg_init_kernel<<<nb, RT, 0, st>>>(f, mask, dinv, minv, r, p, x, n, partial);
+  reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
+  return cuda_status(cudaGetLastError(), "axhelm_cg_init");
+}
+
+int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* mask,
+                     const double* dinv, const double* minv, const double* sc, int64_t n,
+                     double* partial, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = red_blocks(n);
+  cg_update_kernel<<<nb, RT, 0, st>>>(x, r, p, w, mask, dinv, minv, sc, n, partial);
+  reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
+  return cuda_status(cudaGetLastError(), "axhelm_cg_update");
+}
+
+int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const double* sc_new,
+                      const double* sc_old, int64_t n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cg_pupdate_kernel<<<red_blocks(n), RT, 0, st>>>(p, r, dinv, sc_new, sc_old, n);
+  return cuda_status(cudaGetLastError(), "axhelm_cg_pupdate");
+}
+
+int axhelm_diag(double* diag, const double* dxd, const double* dyd, const double* dzd,
+                const double* dxtd, const double* dytd, const double* dztd, const double* h1d,
+                const double* g11d, const double* g22d, const double* g33d, const double* g12d,
+                const double* g13d, const double* g23d, int64_t nel, int lx, void* stream) {
+  if (lx < 2 || lx > 16 || nel < 0) return set_status(AXHELM_EINVAL, "axhelm_diag: bad sizes");
+  const int64_t n = nel * lx * lx * lx;
+  if (n == 0) return set_status(AXHELM_OK, "");
+  AxPtrs A{diag, nullptr, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  diag_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(diag, A, lx, n);
+  return cuda_status(cudaGetLastError(), "axhelm_diag");
+}
+
+}  // extern "C"

@@ -38,19 +38,33 @@ class TorchComm:
         self.dist = dist
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
+        # gloo moves CPU tensors only: stage device buffers through the host
+        # (used to exercise multi-rank runs on a single GPU / CPU-only boxes)
+        self.host_staged = dist.get_backend() == "gloo"
 
     def sendrecv(self, send=None, dst=None, recv=None, src=None):
         d = self.dist
+        s_t, r_t = send, recv
+        if self.host_staged:
+            s_t = send.cpu() if send is not None else None
+            r_t = recv.new_empty(recv.shape, device="cpu") if recv is not None else None
         ops = []
-        if send is not None:
-            ops.append(d.P2POp(d.isend, send, dst))
-        if recv is not None:
-            ops.append(d.P2POp(d.irecv, recv, src))
+        if s_t is not None:
+            ops.append(d.P2POp(d.isend, s_t, dst))
+        if r_t is not None:
+            ops.append(d.P2POp(d.irecv, r_t, src))
         if ops:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
+        if self.host_staged and recv is not None and r_t is not recv:
+            recv.copy_(r_t)
 
     def allreduce_sum(self, t):
+        if self.host_staged and t.device.type != "cpu":
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return t
 

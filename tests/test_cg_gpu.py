@@ -1,0 +1,71 @@
+"""GPU Jacobi-PCG (cg.py) against the NumPy restatement (oracle.pcg) and a
+manufactured solution.  Parity unpinned (the reference has no solver,
+SPEC.md:14): iterates agree to FP64 reassociation; the solve converges."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    if not t.cuda.is_available():
+        pytest.fail("CUDA device required")
+    return t
+
+
+def _setup(torch, nx, ny, nz, lx, mode="strict"):
+    from paper_2506_20994_b200.cg import JacobiPCG
+    from paper_2506_20994_b200.mesh import BoxMesh
+    from paper_2506_20994_b200.operator import HelmholtzOperator
+
+    m = BoxMesh(nx, ny, nz, lx)
+    op = HelmholtzOperator(m, torch, "cuda", mode=mode, amp=0.1)
+    return m, op, JacobiPCG(op)
+
+
+def test_diagonal_matches_unit_vector_applies(torch):
+    m, op, pcg = _setup(torch, 2, 2, 2, 4)
+    arrays = {k: v.cpu().numpy() for k, v in {**op.geom, **op.mats}.items()}
+    arrays["ud"] = np.zeros(m.shape)
+    want = o.dssum(o.local_diag(arrays), o.box_mesh_gid(2, 2, 2, 4))
+    mask = pcg.mask.cpu().numpy()
+    dinv = pcg.dinv.cpu().numpy()
+    got = np.divide(1.0, dinv, out=np.zeros_like(dinv), where=mask > 0)
+    assert o.normwise_rel(got, np.where(mask > 0, want, 0.0)) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,mode", [((3, 2, 2, 4), "strict"), ((2, 2, 3, 5), "fast"), ((2, 2, 2, 8), "fast")])
+def test_pcg_iterates_match_oracle(torch, dims, mode):
+    nx, ny, nz, lx = dims
+    m, op, pcg = _setup(torch, nx, ny, nz, lx, mode)
+    gid = o.box_mesh_gid(nx, ny, nz, lx)
+    rng = np.random.default_rng(1)
+    # a continuous right-hand side: random per global node
+    fg = rng.standard_normal(int(gid.max()) + 1)
+    f = fg[gid]
+    x, hist = pcg.solve(torch.from_numpy(f).cuda(), iters=25)
+    arrays = {k: v.cpu().numpy() for k, v in {**op.geom, **op.mats}.items()}
+    arrays["ud"] = np.zeros(m.shape)
+    xw, hw = o.pcg(arrays, gid, pcg.mask.cpu().numpy(), f, 25)
+    h = hist.cpu().numpy()
+    assert np.max(np.abs(h - hw) / hw) <= 1e-8
+    assert o.normwise_rel(x.cpu().numpy(), xw) <= 1e-9
+
+
+def test_pcg_converges_to_manufactured_solution(torch):
+    nx, ny, nz, lx = 3, 3, 3, 6
+    m, op, pcg = _setup(torch, nx, ny, nz, lx, "fast")
+    gid = m.gid(torch, "cuda")
+    xs = torch.randn(int(gid.max()) + 1, dtype=torch.float64, device="cuda")[gid] * pcg.mask
+    f = torch.empty_like(xs)
+    op.apply(xs, f)
+    x, hist = pcg.solve(f, iters=300)
+    h = hist.cpu().numpy()
+    assert h[-1] <= 1e-20 * h[0]
+    assert float((x - xs).abs().max() / xs.abs().max()) <= 1e-8
