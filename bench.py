@@ -292,22 +292,48 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def mesh_dims(nel):
+    """(nx, ny, nz_per_rank) of the per-rank slab: 64 x 64 x (nel/4096) for
+    the C2 / C4 sizes (2^18 = 64^3 elements per GPU)."""
+    if nel % 4096 == 0:
+        return 64, 64, nel // 4096
+    return 1, 1, nel
+
+
 def ours_arm(args):
     import torch
 
     ws, rank, local = dist_env()
+    comm = None
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local if ws > 1 else 0)
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(local % ndev)
+        backend = os.environ.get("AXHELM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
+        else:
+            dist.init_process_group(backend)
+        from paper_2506_20994_b200.dist import TorchComm
+
+        comm = TorchComm(dist)
+    device = torch.device("cuda", local % torch.cuda.device_count() if ws > 1 else 0)
     torch.cuda.set_device(device)
     from paper_2506_20994_b200 import _lib, kernelrt
+    from paper_2506_20994_b200.mesh import BoxMesh
+    from paper_2506_20994_b200.operator import HelmholtzOperator
 
     lib = _lib.load()
     lx, nel = args.lx, args.nel
-    arr = device_problem(torch, nel, lx, device, seed=1234 + rank)
+    nx, ny, nzr = mesh_dims(nel)
+    mesh = BoxMesh(nx, ny, nzr * ws, lx, rank, ws)
+    assert mesh.nel == nel
+    op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1)
+    g = torch.Generator(device=device).manual_seed(1234 + rank)
+    u = torch.randn(mesh.shape, dtype=torch.float64, device=device, generator=g)
+    w = torch.empty_like(u)
+    arr = {"wd": w, "ud": u, **op.mats, **op.geom}
     stream = torch.cuda.current_stream(device)
     ptrs = [arr[n].data_ptr() for n in ABI]
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -317,19 +343,13 @@ def ours_arm(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def timed(mode_name, steps, warmup, sample_clocks):
-        """W warm-up + K timed applies; CUDA events per launch on the launch stream."""
-        mode = kernelrt.MODES[mode_name]
-
-        def step():
-            rc = lib.axhelm_apply(*ptrs, nel, lx, mode, sp)
-            if rc:
-                raise RuntimeError(_lib.last_error(lib))
-
+    def timed_fn(step, steps, warmup, sample_clocks):
+        """W warm-up + K timed steps between CUDA events on the launch stream;
+        per-step events too (one kernel per ax step -> kernel duration)."""
         for _ in range(max(warmup, 3)):
             step()
         torch.cuda.synchronize()
-        clocks = ClockSampler(torch.cuda.current_device()) if sample_clocks else None
+        clocks = ClockSampler(device.index) if sample_clocks else None
         if clocks:
             time.sleep(0.15)
         barrier()
@@ -347,35 +367,88 @@ def ours_arm(args):
         barrier()
         clk = clocks.stop(t_wall0, time.time()) if clocks else None
         total_ms = start.elapsed_time(end)
-        kern_ms = [a.elapsed_time(b) for a, b in ev]
-        if ws > 1:
-            t = torch.tensor([total_ms], device=device)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            total_ms = float(t.item())
-        return total_ms, kern_ms, clk
+        each = [a.elapsed_time(b) for a, b in ev]
+        return maxrank_ms(total_ms), each, clk
 
-    total_ms, kern_ms, clk = timed(args.mode, args.steps, args.warmup, True)
+    def maxrank_ms(ms):
+        if ws == 1:
+            return ms
+        t = torch.tensor([ms], dtype=torch.float64)
+        if not comm.host_staged:
+            t = t.to(device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def ax_step(mode):
+        m = kernelrt.MODES[mode]
+
+        def step():
+            rc = lib.axhelm_apply(*ptrs, nel, lx, m, sp)
+            if rc:
+                raise RuntimeError(_lib.last_error(lib))
+
+        return step
+
+    pts = nel * lx ** 3
+    total_ms, kern_ms, clk = timed_fn(ax_step(args.mode), args.steps, args.warmup, True)
     other = None
     if not args.no_other_mode:
         om = "strict" if args.mode == "fast" else "fast"
-        o_total, o_kern, o_clk = timed(om, args.steps, args.warmup, True)
+        o_total, o_kern, o_clk = timed_fn(ax_step(om), args.steps, args.warmup, True)
         o_ms = o_total / args.steps
         other = {"mode": om, "ms_per_step": round(o_ms, 5),
-                 "gdof_s": round(nel * lx ** 3 * ws / (o_ms * 1e-3) / 1e9, 4),
-                 "hbm_gbs": round(BYTES_PER_POINT * nel * lx ** 3 / (statistics.fmean(o_kern) * 1e-3) / 1e9, 2),
+                 "gdof_s": round(pts * ws / (o_ms * 1e-3) / 1e9, 4),
+                 "hbm_gbs": round(BYTES_PER_POINT * pts / (statistics.fmean(o_kern) * 1e-3) / 1e9, 2),
                  "clocks": o_clk}
 
     # fast mode's distance from the bit-exact strict result on this data
     # (normwise, the reference's relaxed-fp measure: tests/test_codegen.py:186)
-    fast_vs_strict = None
-    for m in ("strict", "fast"):
-        assert lib.axhelm_apply(*ptrs, nel, lx, kernelrt.MODES[m], sp) == 0
-        if m == "strict":
-            w_strict = arr["wd"].clone()
+    for m_ in ("strict", "fast"):
+        ax_step(m_)()
+        if m_ == "strict":
+            w_strict = w.clone()
     torch.cuda.synchronize()
-    fast_vs_strict = float((arr["wd"] - w_strict).abs().max() / w_strict.abs().max())
+    fast_vs_strict = float((w - w_strict).abs().max() / w_strict.abs().max())
     del w_strict
-    pts = nel * lx ** 3
+
+    # ---- assembled operator: ax + DSSUM (+ NCCL interface exchange)  [C4 per GPU]
+    gs_line = None
+    if not args.no_gs:
+        g_total, _, _ = timed_fn(lambda: op.apply(u, w), args.gs_steps, 3, False)
+        g_ms = g_total / args.gs_steps
+        gs_line = {"workload": f"w = QQ^T A u on a {mesh.nx}x{mesh.ny}x{mesh.nz} brick "
+                               f"(z-slab of {mesh.ez1 - mesh.ez0} layers per rank), lx={lx}",
+                   "steps": args.gs_steps, "ms_per_step": round(g_ms, 5),
+                   "gdof_s": round(pts * ws / (g_ms * 1e-3) / 1e9, 4),
+                   "dssum_ms": round(g_ms - total_ms / args.steps, 5),
+                   "exchange": ("NCCL P2P planes, overlapped with interior ax" if ws > 1 and not
+                                comm.host_staged else ("gloo host-staged planes" if ws > 1 else "none (1 rank)")),
+                   "plane_bytes": mesh.plane * 8}
+
+    # ---- Jacobi-PCG, 100 iterations  [C5 per GPU]
+    cg_line = None
+    if not args.no_cg:
+        from paper_2506_20994_b200.cg import JacobiPCG
+
+        del g
+        pcg = JacobiPCG(op)
+        f = torch.empty_like(u)
+        op.apply(u * pcg.mask, f)
+        pcg.solve(f, iters=3)  # warm-up
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, hist = pcg.solve(f, iters=args.cg_iters)
+        e1.record(stream)
+        barrier()
+        c_ms = maxrank_ms(e0.elapsed_time(e1))
+        h = hist.cpu()
+        cg_line = {"iters": args.cg_iters, "ms_total": round(c_ms, 3),
+                   "ms_per_iter": round(c_ms / args.cg_iters, 5),
+                   "gdof_s_per_iter": round(pts * ws * args.cg_iters / (c_ms * 1e-3) / 1e9, 4),
+                   "rr_reduction": float(h[-1] / h[0])}
+        del pcg, f
+
     ms_step = total_ms / args.steps
     value = pts * ws / (ms_step * 1e-3) / 1e9
     mean_kernel_ms = statistics.fmean(kern_ms)
@@ -402,10 +475,12 @@ def ours_arm(args):
         "metric": "ax_helm GDOF/s", "value": round(value, 4), "unit": "GDOF/s",
         "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated SPD metric, N(0,1) u)",
-        "config": {"workload": f"ax_helm lx={lx}, {nel} elements per GPU (BASELINE config C2)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: deformed-hex brick geometry generated on the device, u ~ N(0,1)",
+        "config": {"workload": f"ax_helm lx={lx}, {nel} elements per GPU (BASELINE C2; z-slab of a "
+                               f"{mesh.nx}x{mesh.ny}x{mesh.nz} brick)",
                    "lx": lx, "nel_per_gpu": nel, "mode": args.mode,
-                   "parallelism": f"element slabs x{ws} (no collective)",
+                   "parallelism": f"element z-slabs x{ws}",
                    "l2": "inputs 9.66 GB/GPU >> 126 MB L2 (no flush needed)"},
         "hbm_gbs": round(achieved, 2),
         "hbm_frac_of_measured": round(achieved / peak, 4),
@@ -419,6 +494,7 @@ def ours_arm(args):
                      "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": args.steps,
         "other_mode": other, "fast_vs_strict_normwise": fast_vs_strict,
+        "ax_plus_gs": gs_line, "pcg": cg_line,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
@@ -493,6 +569,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gs", action="store_true", help="skip the ax + DSSUM measurement")
+    ap.add_argument("--gs-steps", type=int, default=50)
+    ap.add_argument("--no-cg", action="store_true", help="skip the Jacobi-PCG measurement")
+    ap.add_argument("--cg-iters", type=int, default=100)
     ap.add_argument("--cpu-nel", type=int, default=CPU_SAMPLE_NEL)
     ap.add_argument("--cpu-reps", type=int, default=9)
     ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
