@@ -246,7 +246,7 @@ def kernel_name(lx, mode):
     if v == "auto":
         if lx == 8 and mode == "fast":
             return "ax_dmma8 (FP64 DMMA m8n8k4, TMA ring)"
-        if lx <= 8:
+        if lx <= 12:
             return f"ax_tma2<{lx},{mode}> (TMA ring, FP64 vector)"
         return f"ax_kwalk_pf<{lx},{mode}> (L2-prefetch k-walk)"
     return f"AXHELM_KERNEL={v}"

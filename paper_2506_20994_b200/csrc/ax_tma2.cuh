@@ -35,18 +35,58 @@ struct TParams {
   double ztT[LX * LX];  // ztT[k][l] = dztd[l][k]
 };
 
+// Per-lx shape: elements per group (EPL) so a CTA has ~100-300 threads, and
+// the default k-split (NKS).  lx 9..12 run one element per CTA-iteration
+// with a 2 x (8 x lx^3 x 8 B) ring (up to 221 KiB at lx = 12).
+template <int LX>
+struct T2Shape {
+  static constexpr int EPL = LX == 2 ? 32 : LX == 3 ? 14 : LX == 4 ? 8 : LX == 5 ? 5
+                           : LX == 6 ? 3 : LX == 7 ? 2 : 1;
+  static constexpr int NKS = LX >= 8 ? 2 : 1;
+};
+
 template <int LX, int NKS>
 struct T2Cfg {
   static constexpr int L2 = LX * LX;
   static constexpr int L3 = LX * LX * LX;
-  static constexpr int EPL = TCfg<LX>::EPL;
+  static constexpr int EPL = T2Shape<LX>::EPL;
   static constexpr int KS = (LX + NKS - 1) / NKS;
   static constexpr int NT = EPL * L2 * NKS;
   static constexpr int D = 2;
   static constexpr int FIELD = EPL * L3;
-  static constexpr int BUF = 8 * FIELD;
+  // per-field stride in the ring: room for one leading pad double (a group
+  // whose first element starts 8 B past a 16-B boundary is copied from the
+  // aligned address below it) and 16-B alignment of every field
+  static constexpr int FSTRIDE = (FIELD + 2 + 1) & ~1;
+  static constexpr int BUF = 8 * FSTRIDE;
   static constexpr size_t SMEM = 128 + sizeof(double) * (D * BUF + 2 * L2);
 };
+
+// Start loading group g into buf.  Each field's run [e0*L3, e1*L3) is fetched
+// as the 16-B aligned superset [floor16, ceil16) — one cp.async.bulk per
+// field — so odd lx^3 needs no even-element grouping; the data then sits
+// `pad` (0 or 1) doubles into the field's slot.  A superset that would read
+// past the end of the arrays (last group, odd total) falls back to a plain
+// arrive + cooperative load.  Returns pad, or -1 for the fallback.
+template <int LX, int NKS>
+__device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
+                                            uint64_t* bar) {
+  using C = T2Cfg<LX, NKS>;
+  const int64_t e0 = g * C::EPL;
+  const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
+  const int64_t first = e0 * C::L3, last = (e0 + ne) * C::L3;  // doubles
+  const int pad = (int)(first & 1);
+  const int64_t lo = first - pad, hi = (last + 1) & ~(int64_t)1;
+  if (hi > nel * C::L3) {  // would read past the arrays
+    mbar_arrive(bar);
+    return -1;
+  }
+  const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+  mbar_arrive_expect_tx(bar, 8u * bytes);
+#pragma unroll
+  for (int f = 0; f < 8; ++f) bulk_g2s(buf + f * C::FSTRIDE, field_ptr(A, f) + lo, bytes, bar);
+  return pad;
+}
 
 // matrix entry source: kernel parameters (constant bank) or shared memory
 template <int LX, bool UP>
@@ -215,7 +255,7 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
 #pragma unroll
     for (int d = 0; d < C::D; ++d) {
       const int64_t g = blockIdx.x + d * stride;
-      if (g < ngroups) issue_group<LX>(A, nel, g, bufs + d * C::BUF, &bars[d]);
+      if (g < ngroups) issue_group2<LX, NKS>(A, nel, g, bufs + d * C::BUF, &bars[d]);
     }
   }
   // device copy of the t-direction matrices (transposed) + verification of
@@ -249,18 +289,22 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
     const int64_t e0 = g * C::EPL;
     const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
     mbar_wait(&bars[b], parity);
-    if (((ne * L3 * 8) & 15) != 0) {  // cooperative load of an odd-sized tail group
+    // the same pad rule as issue_group2 (recomputed: every thread needs it)
+    int pad = (int)((e0 * L3) & 1);
+    if ((((e0 + ne) * L3 + 1) & ~(int64_t)1) > nel * L3) {  // fallback group: load it ourselves
+      pad = 0;
       for (int f = 0; f < 8; ++f) {
         const double* src = field_ptr(A, f) + e0 * L3;
-        for (int q = tid; q < ne * L3; q += C::NT) buf[f * FIELD + q] = src[q];
+        for (int q = tid; q < ne * L3; q += C::NT) buf[f * C::FSTRIDE + q] = src[q];
       }
       __syncthreads();
     }
     const bool active = el < ne;
-    const int eoff = el * L3;
-    ElemView v{buf + 0 * FIELD + eoff, buf + 1 * FIELD + eoff, buf + 2 * FIELD + eoff,
-               buf + 3 * FIELD + eoff, buf + 4 * FIELD + eoff, buf + 5 * FIELD + eoff,
-               buf + 6 * FIELD + eoff, buf + 7 * FIELD + eoff};
+    const int eoff = el * L3 + pad;
+    constexpr int FS = C::FSTRIDE;
+    ElemView v{buf + 0 * FS + eoff, buf + 1 * FS + eoff, buf + 2 * FS + eoff,
+               buf + 3 * FS + eoff, buf + 4 * FS + eoff, buf + 5 * FS + eoff,
+               buf + 6 * FS + eoff, buf + 7 * FS + eoff};
     double utr[LX];
     if (use_param) stage1_dispatch<LX, FAST, NKS, true>(kh, P, sZ, v, dxr, dyr, j, i, utr);
     else stage1_dispatch<LX, FAST, NKS, false>(kh, P, sZ, v, dxr, dyr, j, i, utr);
@@ -273,7 +317,7 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
       const int64_t gn = g + C::D * stride;
       if (gn < ngroups) {
         fence_proxy_async();
-        issue_group<LX>(A, nel, gn, buf, &bars[b]);
+        issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
       }
     }
   }

@@ -302,14 +302,14 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
     if (g_variant == 5 && aligned16(A)) {
       if constexpr (LX == 8) return launch_row<LX, FAST>(A, nel, st, hx, hxt);
     }
-    if ((g_variant >= 4 || g_variant == 0) && aligned16(A)) {
+  }
+  if constexpr (LX <= 12) {
+    if ((g_variant >= 3 || g_variant == 0) && aligned16(A)) {
       if constexpr (LX == 8) {
         if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
         if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
-        return launch_tma2<LX, FAST, 2>(A, nel, st, hz, hzt);
-      } else {
-        return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
       }
+      return launch_tma2<LX, FAST, T2Shape<LX>::NKS>(A, nel, st, hz, hzt);
     }
   }
   if constexpr (LX == 8) {
