@@ -142,14 +142,24 @@ int axhelm_reduce_blocks(int64_t n);
 /* out[0] = sum a*b (times wt if non-NULL) */
 int axhelm_dot(const double* a, const double* b, const double* wt, int64_t n, double* partial,
                double* out, void* stream);
-/* r = mask*f, p = dinv*r, x = 0; out = {sum minv r dinv r, sum minv r r} */
-int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* minv,
+/* r = mask*f, p = dinv*r, x = 0; out = {sum cwt r dinv r, sum cwt r r}
+ * with cwt = mask / multiplicity (each interior node counted once) */
+int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* cwt,
                    double* r, double* p, double* x, int64_t n, double* partial, double* out,
                    void* stream);
-/* alpha = sc[0]/sc[1]; x += alpha p; r -= alpha mask w; out = {rz, rr} */
-int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* mask,
-                     const double* dinv, const double* minv, const double* sc, int64_t n,
-                     double* partial, double* out, void* stream);
+/* alpha = sc[0]/sc[1]; x += alpha p; r -= alpha w; out = {rz, rr} (weights cwt) */
+int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* dinv,
+                     const double* cwt, const double* sc, int64_t n, double* partial, double* out,
+                     void* stream);
+/* w = A_local u (element-local ax_helm, no DSSUM) and out[0] = sum u*w over
+ * the local points, fused into the FP64-DMMA kernel for lx = 8 fast mode.
+ * For a continuous u vanishing where the mask does, this equals the
+ * assembled <u, mask QQ^T A u> (each node once) — the PCG's p.Ap. */
+int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int64_t nel,
+                     int lx, int mode, double* partial, double* out, void* stream);
 /* p = dinv r + (sc_new[0]/sc_old[0]) p */
 int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const double* sc_new,
                       const double* sc_old, int64_t n, void* stream);

@@ -36,7 +36,8 @@ PROTOTYPES = {
     "axhelm_reduce_blocks": (ctypes.c_int, [ctypes.c_int64]),
     "axhelm_dot": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "axhelm_cg_init": (ctypes.c_int, [_vp] * 7 + [ctypes.c_int64, _vp, _vp, _vp]),
-    "axhelm_cg_update": (ctypes.c_int, [_vp] * 8 + [ctypes.c_int64, _vp, _vp, _vp]),
+    "axhelm_cg_update": (ctypes.c_int, [_vp] * 7 + [ctypes.c_int64, _vp, _vp, _vp]),
+    "axhelm_apply_dot": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "axhelm_cg_pupdate": (ctypes.c_int, [_vp] * 5 + [ctypes.c_int64, _vp]),
     "axhelm_diag": (ctypes.c_int, [_vp] * 14 + [ctypes.c_int64, ctypes.c_int, _vp]),
     "axhelm_set_mode": (ctypes.c_int, [ctypes.c_int]),

@@ -10,10 +10,16 @@ node); global inner products weight each copy by 1/multiplicity so every
 node counts once:  <a, b> = sum_p a_p b_p / mult_p  (all-reduced over ranks).
 
 One iteration (no host synchronisation; scalars live in device memory):
-  w  = mask . Q Q^T A p                     (operator.apply)
-  pw = <p, w>                               (axhelm_dot + all-reduce)
-  x += a p ; r -= a mask w ; rz', rr        (axhelm_cg_update + all-reduce)
+  w  = Q Q^T A p,  pw = sum_p p (A p)       (operator.apply: the dot is fused
+                                             into the lx=8 DMMA kernel and taken
+                                             before assembly, = <p, mask QQ^T A p>
+                                             since p is continuous and vanishes
+                                             on the boundary; + all-reduce)
+  x += a p ; r -= a w ; rz', rr             (axhelm_cg_update, weights
+                                             cwt = mask/mult; + all-reduce)
   p  = dinv r + (rz'/rz) p                  (axhelm_cg_pupdate)
+r is left unmasked on the boundary: only dinv*r and cwt-weighted sums read
+it, and both vanish there.
 """
 
 from __future__ import annotations
@@ -47,7 +53,7 @@ class JacobiPCG:
         # multiplicity (DSSUM of ones, across ranks) and the Jacobi diagonal
         mult = torch.ones(m.shape, **f64)
         op.dssum(mult)
-        self.minv = (1.0 / mult).contiguous()
+        self.cwt = (self.mask / mult).contiguous()
         del mult
         diag = torch.empty(m.shape, **f64)
         g = op.geom
@@ -87,25 +93,22 @@ class JacobiPCG:
         n = self.n
         # per-iteration scalar slots: sc[i] = (rz_i, rr_i), pw[i]
         sc = torch.zeros(iters + 1, 2, dtype=torch.float64, device=dev)
-        pw = torch.zeros(iters, 1, dtype=torch.float64, device=dev)
         s = self._s()
         x, r, p, w = self.x, self.r, self.p, self.w
         P = self.partial.data_ptr()
         self._check(self.lib.axhelm_cg_init(f.data_ptr(), self.mask.data_ptr(), self.dinv.data_ptr(),
-                                            self.minv.data_ptr(), r.data_ptr(), p.data_ptr(),
+                                            self.cwt.data_ptr(), r.data_ptr(), p.data_ptr(),
                                             x.data_ptr(), n, P, sc[0].data_ptr(), s))
         self._allreduce(sc[0])
+        # (rz_i, pw_i) side by side for the update kernel
+        a = torch.zeros(iters, 2, dtype=torch.float64, device=dev)
         for it in range(iters):
-            self.op.apply(p, w)
-            self._check(self.lib.axhelm_dot(p.data_ptr(), w.data_ptr(), self.minv.data_ptr(), n, P,
-                                            pw[it].data_ptr(), s))
-            self._allreduce(pw[it])
-            # update reads (rz, pw) as a 2-vector: stage them contiguously
-            a = torch.stack((sc[it, 0], pw[it, 0]))
+            a[it, 0:1].copy_(sc[it, 0:1])
+            self.op.apply(p, w, dot=a[it, 1:2])
+            self._allreduce(a[it, 1:2])
             self._check(self.lib.axhelm_cg_update(x.data_ptr(), r.data_ptr(), p.data_ptr(), w.data_ptr(),
-                                                  self.mask.data_ptr(), self.dinv.data_ptr(),
-                                                  self.minv.data_ptr(), a.data_ptr(), n, P,
-                                                  sc[it + 1].data_ptr(), s))
+                                                  self.dinv.data_ptr(), self.cwt.data_ptr(),
+                                                  a[it].data_ptr(), n, P, sc[it + 1].data_ptr(), s))
             self._allreduce(sc[it + 1])
             self._check(self.lib.axhelm_cg_pupdate(p.data_ptr(), r.data_ptr(), self.dinv.data_ptr(),
                                                    sc[it + 1].data_ptr(), sc[it].data_ptr(), n, s))

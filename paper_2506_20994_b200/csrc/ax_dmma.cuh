@@ -56,8 +56,11 @@ __device__ __forceinline__ int ut_idx(int l, int j, int i) {
   return l * 64 + ((j ^ (l & 1)) << 3) + (i ^ (((l >> 1) & 1) << 2));
 }
 
+// DOT: also accumulate sum_p u_p w_p over the CTA's elements (in a fixed
+// order) into dot_partial[blockIdx.x] — the PCG's <p, A p> without a pass.
+template <bool DOT>
 __global__ void __launch_bounds__(DmCfg::NT)
-ax_dmma8(const AxPtrs A, const int64_t nel) {
+ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
   using C = DmCfg;
   constexpr int FIELD = C::FIELD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -100,6 +103,7 @@ ax_dmma8(const AxPtrs A, const int64_t nel) {
     fzt[s] = A.dzt[(q + 4 * s) * 8 + g];
   }
 
+  double dot_acc = 0.0;
   int64_t n = 0;
   for (int64_t e = blockIdx.x; e < nel; e += stride, ++n) {
     const int b = (int)(n % C::D);
@@ -141,6 +145,15 @@ ax_dmma8(const AxPtrs A, const int64_t nel) {
 
     // ---- phase B: combine at the own points (k, g, 2q..2q+1)
     double ur[4][2], us[4][2], ut[4][2];
+    double uown[4][2];  // DOT: u at the own points (U is overwritten below)
+    if constexpr (DOT) {
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt) {
+        const double2 uu = lds2(U + (warp * 4 + kt) * 64 + g * 8 + 2 * q);
+        uown[kt][0] = uu.x;
+        uown[kt][1] = uu.y;
+      }
+    }
 #pragma unroll
     for (int kt = 0; kt < 4; ++kt) {
       const int k = warp * 4 + kt;
@@ -200,9 +213,10 @@ ax_dmma8(const AxPtrs A, const int64_t nel) {
       const int k = warp * 4 + kt;
       const int o = k * 64 + g * 8 + 2 * q;
       const double2 z = lds2(ST + o);
-      asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(wout + o), "d"(w[kt][0] + z.x),
-                   "d"(w[kt][1] + z.y)
+      const double w0 = w[kt][0] + z.x, w1 = w[kt][1] + z.y;
+      asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(wout + o), "d"(w0), "d"(w1)
                    : "memory");
+      if constexpr (DOT) dot_acc = fma(uown[kt][0], w0, fma(uown[kt][1], w1, dot_acc));
     }
     __syncthreads();  // buffer b and ST free
     if (tid == 0) {
@@ -211,6 +225,18 @@ ax_dmma8(const AxPtrs A, const int64_t nel) {
         fence_proxy_async();
         issue_group<8>(A, nel, en, buf, &bars[b]);
       }
+    }
+  }
+  if constexpr (DOT) {
+    // fixed-order CTA reduction of the per-thread sums
+    double* red = ST;  // free after the loop
+    __syncthreads();
+    red[tid] = dot_acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q2 = 0; q2 < C::NT; ++q2) t += red[q2];
+      dot_partial[blockIdx.x] = t;
     }
   }
 }

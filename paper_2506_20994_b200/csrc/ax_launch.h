@@ -20,6 +20,12 @@ cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream
                       const double* hz = nullptr, const double* hzt = nullptr,
                       const double* hx = nullptr, const double* hxt = nullptr);
 
+// fused lx = 8 fast apply + per-CTA partials of sum u*w (nparts written)
+cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int* nparts,
+                             cudaStream_t st);
+// true when launch_ax would run the fused-capable DMMA kernel
+bool dmma8_selected(const AxPtrs& A, int lx, int mode);
+
 // __dace_ax_helm body: classify the 15 pointers (device / pinned host /
 // pageable host) and run the apply synchronously, staging host data through
 // the GPU in copy/compute-overlapped chunks.

@@ -87,6 +87,7 @@ static int g_pf = [] {
   return (d >= 1 && d <= 3) ? d : 1;
 }();
 static int g_num_sms = 0;
+static bool aligned16(const AxPtrs& A);
 
 static int num_sms() {
   if (g_num_sms == 0) {
@@ -243,21 +244,47 @@ static cudaError_t launch_row(const AxPtrs& A, int64_t nel, cudaStream_t st, con
   return cudaGetLastError();
 }
 
-static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+static int dmma8_grid(int64_t nel, cudaError_t* err) {
   using C = DmCfg;
   static int blocks_per_sm = 0;
+  *err = cudaSuccess;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(ax_dmma8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
-    if (e != cudaSuccess) return e;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ax_dmma8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_dmma8, C::NT, C::SMEM);
-    if (e != cudaSuccess) return e;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_dmma8<true>, C::NT, C::SMEM);
+    if (e != cudaSuccess) {
+      *err = e;
+      return 0;
+    }
     blocks_per_sm = b > 0 ? b : 1;
   }
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
-  if (grid > nel) grid = nel;
-  ax_dmma8<<<(unsigned)grid, C::NT, C::SMEM, st>>>(A, nel);
+  return (int)(grid > nel ? nel : grid);
+}
+
+static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+  cudaError_t e;
+  const int grid = dmma8_grid(nel, &e);
+  if (e != cudaSuccess) return e;
+  ax_dmma8<false><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, nullptr);
+  return cudaGetLastError();
+}
+
+bool dmma8_selected(const AxPtrs& A, int lx, int mode) {
+  return lx == 8 && mode == AXHELM_FAST && (g_variant == 0 || g_variant == 6) && aligned16(A);
+}
+
+// fused apply + sum u*w (lx = 8, fast): per-CTA partials, fixed-order reduce
+cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int* nparts,
+                             cudaStream_t st) {
+  cudaError_t e;
+  const int grid = dmma8_grid(nel, &e);
+  if (e != cudaSuccess) return e;
+  ax_dmma8<true><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial);
+  *nparts = grid;
   return cudaGetLastError();
 }
 

@@ -63,9 +63,9 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
   write_partials<1>(v, partial);
 }
 
-// r = mask*f ; p = dinv*r ; partial: rz = sum minv r dinv r, rr = sum minv r r
+// r = mask*f ; p = dinv*r ; partial: rz = sum cwt r dinv r, rr = sum cwt r r
 __global__ void cg_init_kernel(const double* __restrict__ f, const double* __restrict__ mask,
-                               const double* __restrict__ dinv, const double* __restrict__ minv,
+                               const double* __restrict__ dinv, const double* __restrict__ cwt,
                                double* __restrict__ r, double* __restrict__ p,
                                double* __restrict__ x, int64_t n, double* __restrict__ partial) {
   double v[2] = {0.0, 0.0};
@@ -75,27 +75,30 @@ __global__ void cg_init_kernel(const double* __restrict__ f, const double* __res
     r[q] = rr;
     p[q] = z;
     x[q] = 0.0;
-    v[0] += minv[q] * rr * z;
-    v[1] += minv[q] * rr * rr;
+    v[0] += cwt[q] * rr * z;
+    v[1] += cwt[q] * rr * rr;
   }
   write_partials<2>(v, partial);
 }
 
-// alpha = sc[0] / sc[1] (rz / pw); x += alpha p; r -= alpha mask w;
-// partial: rz' = sum minv r dinv r, rr = sum minv r r
+// alpha = sc[0] / sc[1] (rz / pw); x += alpha p; r -= alpha w;
+// partial: rz' = sum cwt r dinv r, rr = sum cwt r r, cwt = mask / multiplicity.
+// r is not masked: its boundary values are never used (dinv and cwt vanish
+// there, and p = dinv r + beta p stays zero on the boundary).
 __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
                                  const double* __restrict__ p, const double* __restrict__ w,
-                                 const double* __restrict__ mask, const double* __restrict__ dinv,
-                                 const double* __restrict__ minv, const double* __restrict__ sc,
-                                 int64_t n, double* __restrict__ partial) {
+                                 const double* __restrict__ dinv, const double* __restrict__ cwt,
+                                 const double* __restrict__ sc, int64_t n,
+                                 double* __restrict__ partial) {
   const double alpha = sc[0] / sc[1];
   double v[2] = {0.0, 0.0};
   for (int64_t q = (int64_t)blockIdx.x * RT + threadIdx.x; q < n; q += (int64_t)gridDim.x * RT) {
     x[q] = fma(alpha, p[q], x[q]);
-    const double rr = fma(-alpha, mask[q] * w[q], r[q]);
+    const double rr = fma(-alpha, w[q], r[q]);
     r[q] = rr;
-    v[0] += minv[q] * rr * dinv[q] * rr;
-    v[1] += minv[q] * rr * rr;
+    const double c = cwt[q] * rr;
+    v[0] += c * dinv[q] * rr;
+    v[1] += c * rr;
   }
   write_partials<2>(v, partial);
 }
@@ -162,22 +165,22 @@ int axhelm_dot(const double* a, const double* b, const double* wt, int64_t n, do
   return cuda_status(cudaGetLastError(), "axhelm_dot");
 }
 
-int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* minv,
+int axhelm_cg_init(const double* f, const double* mask, const double* dinv, const double* cwt,
                    double* r, double* p, double* x, int64_t n, double* partial, double* out,
                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
-  cg_init_kernel<<<nb, RT, 0, st>>>(f, mask, dinv, minv, r, p, x, n, partial);
+  cg_init_kernel<<<nb, RT, 0, st>>>(f, mask, dinv, cwt, r, p, x, n, partial);
   reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
   return cuda_status(cudaGetLastError(), "axhelm_cg_init");
 }
 
-int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* mask,
-                     const double* dinv, const double* minv, const double* sc, int64_t n,
-                     double* partial, double* out, void* stream) {
+int axhelm_cg_update(double* x, double* r, const double* p, const double* w, const double* dinv,
+                     const double* cwt, const double* sc, int64_t n, double* partial, double* out,
+                     void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
-  cg_update_kernel<<<nb, RT, 0, st>>>(x, r, p, w, mask, dinv, minv, sc, n, partial);
+  cg_update_kernel<<<nb, RT, 0, st>>>(x, r, p, w, dinv, cwt, sc, n, partial);
   reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
   return cuda_status(cudaGetLastError(), "axhelm_cg_update");
 }
@@ -187,6 +190,35 @@ int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const doub
   cudaStream_t st = (cudaStream_t)stream;
   cg_pupdate_kernel<<<red_blocks(n), RT, 0, st>>>(p, r, dinv, sc_new, sc_old, n);
   return cuda_status(cudaGetLastError(), "axhelm_cg_pupdate");
+}
+
+int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int64_t nel,
+                     int lx, int mode, double* partial, double* out, void* stream) {
+  if (lx < 2 || lx > 16 || nel < 0) return set_status(AXHELM_EINVAL, "axhelm_apply_dot: bad sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  const int64_t n = nel * lx * lx * lx;
+  cudaError_t e;
+  if (nel > 0 && dmma8_selected(A, lx, mode)) {
+    int nb = 0;
+    e = launch_dmma8_dot(A, nel, partial, &nb, st);
+    if (e == cudaSuccess) {
+      reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
+      e = cudaGetLastError();
+    }
+    return cuda_status(e, "axhelm_apply_dot");
+  }
+  e = launch_ax(A, nel, lx, mode, st);
+  if (e == cudaSuccess) {
+    const int nb = red_blocks(n);
+    dot_kernel<<<nb, RT, 0, st>>>(ud, wd, nullptr, n, partial);
+    reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
+    e = cudaGetLastError();
+  }
+  return cuda_status(e, "axhelm_apply_dot");
 }
 
 int axhelm_diag(double* diag, const double* dxd, const double* dyd, const double* dzd,

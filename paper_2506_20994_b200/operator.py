@@ -48,11 +48,15 @@ class HelmholtzOperator:
         self.overlap = overlap and mesh.world > 1 and (mesh.ez1 - mesh.ez0) > 2
         self.side = torch.cuda.Stream(device) if self.overlap else None
         self.L3 = mesh.lx ** 3
+        self._part = {}
+        self._dots = torch.zeros(3, dtype=torch.float64, device=device)
 
     # ----------------------------------------------------------- pieces
 
-    def ax(self, u, w, e0: int = 0, e1: int | None = None, stream=None):
-        """ax_helm on local elements [e0, e1) (stream-ordered)."""
+    def ax(self, u, w, e0: int = 0, e1: int | None = None, stream=None, dot=None):
+        """ax_helm on local elements [e0, e1) (stream-ordered).  dot: a device
+        scalar receiving sum u*w over those elements (fused into the kernel
+        for lx = 8 fast mode)."""
         m = self.mesh
         e1 = m.nel if e1 is None else e1
         n = e1 - e0
@@ -68,26 +72,42 @@ class HelmholtzOperator:
                 p(self.mats["dztd"], False)] + [p(self.geom[f]) for f in FIELDS]
         if stream is None:
             stream = self.torch.cuda.current_stream(self.device)
-        rc = self.lib.axhelm_apply(*ptrs, n, m.lx, self.mode, ctypes.c_void_p(stream.cuda_stream))
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        if dot is None:
+            rc = self.lib.axhelm_apply(*ptrs, n, m.lx, self.mode, sp)
+        else:
+            part = self._partials(stream)
+            rc = self.lib.axhelm_apply_dot(*ptrs, n, m.lx, self.mode, part.data_ptr(), dot.data_ptr(), sp)
         if rc:
             raise DeviceError(_lib.last_error(self.lib))
 
-    def apply(self, u, w):
-        """w = Q Q^T A u on this rank (with the interface exchange)."""
+    def _partials(self, stream):
+        """Per-stream scratch for the fused dot's block partials."""
+        key = stream.cuda_stream
+        if key not in self._part:
+            nb = self.lib.axhelm_reduce_blocks(self.mesh.nel * self.L3)
+            self._part[key] = self.torch.empty(max(nb, 2048), dtype=self.torch.float64, device=self.device)
+        return self._part[key]
+
+    def apply(self, u, w, dot=None):
+        """w = Q Q^T A u on this rank (with the interface exchange).  dot: an
+        optional device scalar receiving the rank-local sum_p u_p (A u)_p
+        before assembly (= <u, QQ^T A u> for continuous u; PCG's p.Ap)."""
         m = self.mesh
         torch = self.torch
         if not self.overlap:
-            self.ax(u, w)
+            self.ax(u, w, dot=dot)
             self.dssum(w)
             return w
         s0 = torch.cuda.current_stream(self.device)
         lay = m.nx * m.ny
+        d3 = self._dots if dot is not None else None
         # boundary element layers first (their results feed the exchange)
-        self.ax(u, w, 0, lay)
-        self.ax(u, w, m.nel - lay, m.nel)
+        self.ax(u, w, 0, lay, dot=d3[0:1] if d3 is not None else None)
+        self.ax(u, w, m.nel - lay, m.nel, dot=d3[1:2] if d3 is not None else None)
         self.side.wait_stream(s0)
         with torch.cuda.stream(self.side):
-            self.ax(u, w, lay, m.nel - lay, stream=self.side)
+            self.ax(u, w, lay, m.nel - lay, stream=self.side, dot=d3[2:3] if d3 is not None else None)
         d = self.dssum
         if d.has_top:
             self.gs.plane(0, "top", w, d.buf_top)
@@ -101,6 +121,8 @@ class HelmholtzOperator:
         d.phase_write(w)
         s0.wait_stream(self.side)
         self.gs.sum_local(w)
+        if dot is not None:
+            dot.copy_(d3.sum().reshape(dot.shape))
         return w
 
     def bytes_per_apply(self) -> int:
