@@ -1,4 +1,6 @@
-// v3 ax_helm kernel: persistent CTAs fed by a TMA bulk-copy ring (sm_100a).
+// TMA bulk-copy ring building blocks (mbarrier, cp.async.bulk, group issue)
+// shared by the v4 / v6 kernels, and the roofline stream probe.  The v3
+// kernel that introduced them (retired, superseded by v4) is described here.
 //
 // Why: the k-walk kernels (v1/v2) load the six geometric factors and h1 into
 // registers, so the bytes in flight per SM are capped by registers x warps;
@@ -136,142 +138,11 @@ __device__ __forceinline__ void lds_row(const double* src, double (&dst)[LX]) {
   }
 }
 
-template <int LX, bool FAST>
-__global__ void __launch_bounds__(TCfg<LX>::NT)
-ax_tma(const AxPtrs A, const int64_t nel) {
-  using C = TCfg<LX>;
-  constexpr int L2 = C::L2, L3 = C::L3, FIELD = C::FIELD;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-  double* bufs = reinterpret_cast<double*>(smem_raw + 128);
-  double* sZ = bufs + C::D * C::BUF;  // sZ[k][l] = dzd[l][k], then dztd likewise
-  double* sZt = sZ + L2;
-
-  const int tid = threadIdx.x;
-  const int el = tid / L2;
-  const int p = tid - el * L2;
-  const int j = p / LX;
-  const int i = p - j * LX;
-  const int64_t ngroups = (nel + C::EPL - 1) / C::EPL;
-  const int64_t stride = gridDim.x;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int d = 0; d < C::D; ++d) mbar_init(&bars[d], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-#pragma unroll
-    for (int d = 0; d < C::D; ++d) {
-      const int64_t g = blockIdx.x + d * stride;
-      if (g < ngroups) issue_group<LX>(A, nel, g, bufs + d * C::BUF, &bars[d]);
-    }
-  }
-
-  for (int q = tid; q < L2; q += C::NT) {
-    const int l = q / LX, k = q - (q / LX) * LX;
-    sZ[k * LX + l] = A.dz[q];
-    sZt[k * LX + l] = A.dzt[q];
-  }
-  __syncthreads();
-
-  double dxr[LX], dyr[LX], dxtr[LX], dytr[LX];
-#pragma unroll
-  for (int l = 0; l < LX; ++l) {
-    dxr[l] = A.dx[l * LX + i];
-    dyr[l] = A.dy[l * LX + j];
-    dxtr[l] = A.dxt[l * LX + i];
-    dytr[l] = A.dyt[l * LX + j];
-  }
-
-  int64_t n = 0;
-  for (int64_t g = blockIdx.x; g < ngroups; g += stride, ++n) {
-    const int b = (int)(n % C::D);
-    const uint32_t parity = (uint32_t)((n / C::D) & 1);
-    double* buf = bufs + b * C::BUF;
-    const int64_t e0 = g * C::EPL;
-    const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
-    mbar_wait(&bars[b], parity);
-    if (((ne * L3 * 8) & 15) != 0) {  // cooperative load of an odd-sized tail group
-      for (int f = 0; f < 8; ++f) {
-        const double* src = field_ptr(A, f) + e0 * L3;
-        for (int q = tid; q < ne * L3; q += C::NT) buf[f * FIELD + q] = src[q];
-      }
-      __syncthreads();
-    }
-    const bool active = el < ne;
-    const int eoff = el * L3;
-    double* U = buf + 0 * FIELD + eoff;
-    double* H = buf + 1 * FIELD + eoff;
-    double* G11 = buf + 2 * FIELD + eoff;  // becomes ur
-    double* G22 = buf + 3 * FIELD + eoff;  // becomes us
-    double* G33 = buf + 4 * FIELD + eoff;
-    double* G12 = buf + 5 * FIELD + eoff;
-    double* G13 = buf + 6 * FIELD + eoff;
-    double* G23 = buf + 7 * FIELD + eoff;
-
-    double ucol[LX];
-#pragma unroll
-    for (int l = 0; l < LX; ++l) ucol[l] = U[l * L2 + p];
-
-    double utr[LX];
-#pragma unroll
-    for (int k = 0; k < LX; ++k) {
-      double urow[LX], uc[LX], dz[LX];
-      lds_row<LX>(U + k * L2 + j * LX, urow);
-      lds_row<LX>(sZ + k * LX, dz);
-#pragma unroll
-      for (int l = 0; l < LX; ++l) uc[l] = U[k * L2 + l * LX + i];
-      double r = 0.0, s = 0.0, t = 0.0;
-#pragma unroll
-      for (int l = 0; l < LX; ++l) {
-        r = madd<FAST>(r, dxr[l], urow[l]);
-        s = madd<FAST>(s, dyr[l], uc[l]);
-        t = madd<FAST>(t, dz[l], ucol[l]);
-      }
-      const int q = k * L2 + p;
-      const double h = H[q], a11 = G11[q], a22 = G22[q], a33 = G33[q];
-      const double a12 = G12[q], a13 = G13[q], a23 = G23[q];
-      G11[q] = combine<FAST>(h, a11, a12, a13, r, s, t);  // ur
-      G22[q] = combine<FAST>(h, a12, a22, a23, r, s, t);  // us
-      utr[k] = combine<FAST>(h, a13, a23, a33, r, s, t);
-    }
-    __syncthreads();  // ur / us of the whole element visible
-
-    double* wout = A.w + (e0 + el) * L3 + p;
-#pragma unroll
-    for (int k = 0; k < LX; ++k) {
-      double rrow[LX], sc[LX], dzt[LX];
-      lds_row<LX>(G11 + k * L2 + j * LX, rrow);
-      lds_row<LX>(sZt + k * LX, dzt);
-#pragma unroll
-      for (int l = 0; l < LX; ++l) sc[l] = G22[k * L2 + l * LX + i];
-      double w = 0.0;
-#pragma unroll
-      for (int l = 0; l < LX; ++l) {
-        w = madd<FAST>(w, dxtr[l], rrow[l]);
-        w = madd<FAST>(w, dytr[l], sc[l]);
-        w = madd<FAST>(w, dzt[l], utr[l]);
-      }
-      if (active) stg_stream(wout + k * L2, w);
-    }
-    __syncthreads();  // every read of buffer b is done
-    if (tid == 0) {
-      const int64_t gn = g + C::D * stride;
-      if (gn < ngroups) {
-        fence_proxy_async();  // order our generic-proxy accesses before the refill
-        issue_group<LX>(A, nel, gn, buf, &bars[b]);
-      }
-    }
-  }
-}
-
 }  // namespace axb
 
 namespace axb {
 
-// Roofline probe: the same TMA ring and the same HBM traffic as ax_tma
+// Roofline probe: the same TMA ring and the same HBM traffic as the apply
 // (8 fields in, w out) with trivial arithmetic (w = sum of the 8 fields).
 // Its time is the memory-side ceiling of the ring design for this
 // read:write mix; exported as axhelm_probe_stream for bench/profiling only.

@@ -13,7 +13,6 @@
 #include "ax_kernels.cuh"
 #include "ax_tma.cuh"
 #include "ax_tma2.cuh"
-#include "ax_row.cuh"
 #include "ax_dmma.cuh"
 #include "ax_launch.h"
 
@@ -66,17 +65,16 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 }
 
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
-// pf (v2, L2-prefetching k-walk), tma (v3, TMA ring), tma2 (v4: v3 +
-// constant-bank dz/dzt + k-split), row (v5, row-per-thread; lx = 8) or
-// dmma (v6, FP64 tensor cores; fast mode, lx = 8).  Default ("auto"): v6 for
-// fast lx = 8, v4 for every other lx <= 8 (16-B aligned fields), else v2.
+// pf (v2, L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
+// + k-split) or dmma (v6, FP64 tensor cores; fast mode, lx = 8).  Default
+// ("auto"): v6 for fast lx = 8, v4 for every other lx <= 12 (16-B aligned
+// fields), else v2.  (v3 = v4 without its refinements and v5 = row per
+// thread were measured and retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
 static int g_variant = [] {
   const char* v = getenv("AXHELM_KERNEL");
   if (v && !strcmp(v, "kwalk")) return 1;
   if (v && !strcmp(v, "pf")) return 2;
-  if (v && !strcmp(v, "tma")) return 3;
-  if (v && !strcmp(v, "row")) return 5;
   if (v && !strcmp(v, "tma2")) return 4;
   if (v && !strcmp(v, "dmma")) return 6;
   return 0;  // auto
@@ -88,6 +86,13 @@ static int g_pf = [] {
 }();
 static int g_num_sms = 0;
 static bool aligned16(const AxPtrs& A);
+// AXHELM_CTAS_PER_SM caps the persistent kernels' resident CTAs per SM
+// (tuning knob; 0 = occupancy limit)
+static int g_cta_cap = [] {
+  const char* v = getenv("AXHELM_CTAS_PER_SM");
+  return v ? atoi(v) : 0;
+}();
+static int cap_ctas(int b) { return (g_cta_cap > 0 && g_cta_cap < b) ? g_cta_cap : b; }
 
 static int num_sms() {
   if (g_num_sms == 0) {
@@ -98,25 +103,6 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int LX, bool FAST>
-static cudaError_t launch_tma(const AxPtrs& A, int64_t nel, cudaStream_t st) {
-  using C = TCfg<LX>;
-  static int blocks_per_sm = 0;  // benign race: idempotent
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_tma<LX, FAST>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma<LX, FAST>, C::NT, C::SMEM);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm = b > 0 ? b : 1;
-  }
-  const int64_t groups = (nel + C::EPL - 1) / C::EPL;
-  int64_t grid = (int64_t)blocks_per_sm * num_sms();
-  if (grid > groups) grid = groups;
-  ax_tma<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(A, nel);
-  return cudaGetLastError();
-}
 
 // ---- host copies of the t-direction matrices for the parameter block (v4)
 //
@@ -194,7 +180,7 @@ static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, co
     int b = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma2<LX, FAST, NKS>, C::NT, C::SMEM);
     if (e != cudaSuccess) return e;
-    blocks_per_sm = b > 0 ? b : 1;
+    blocks_per_sm = cap_ctas(b > 0 ? b : 1);
   }
   TParams<LX> P;
   P.A = A;
@@ -214,35 +200,6 @@ static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, co
   return cudaGetLastError();
 }
 
-template <int LX, bool FAST>
-static cudaError_t launch_row(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hx,
-                              const double* hxt) {
-  using C = RCfg<LX>;
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_row<LX, FAST>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_row<LX, FAST>, C::NT, C::SMEM);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm = b > 0 ? b : 1;
-  }
-  RParams<LX> P;
-  P.A = A;
-  P.nel = nel;
-  // host copies of dxd / dxtd (same cache as v4's dzd / dztd: keyed by pointer)
-  AxPtrs Ax = A;
-  Ax.dz = A.dx;
-  Ax.dzt = A.dxt;
-  cudaError_t e = host_matrices(Ax, LX, hx, hxt, st, P.dx, P.dxt, &P.stale);
-  if (e != cudaSuccess) return e;
-  const int64_t groups = (nel + C::EPL - 1) / C::EPL;
-  int64_t grid = (int64_t)blocks_per_sm * num_sms();
-  if (grid > groups) grid = groups;
-  ax_row<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
-  return cudaGetLastError();
-}
 
 static int dmma8_grid(int64_t nel, cudaError_t* err) {
   using C = DmCfg;
@@ -259,7 +216,7 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
       *err = e;
       return 0;
     }
-    blocks_per_sm = b > 0 ? b : 1;
+    blocks_per_sm = cap_ctas(b > 0 ? b : 1);
   }
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   return (int)(grid > nel ? nel : grid);
@@ -322,16 +279,12 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
                                   const double* hzt, const double* hx, const double* hxt) {
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
   if constexpr (LX <= 8) {
-    if (g_variant == 3 && aligned16(A)) return launch_tma<LX, FAST>(A, nel, st);
     if ((g_variant == 6 || g_variant == 0) && FAST && aligned16(A)) {
       if constexpr (LX == 8) return launch_dmma8(A, nel, st);
     }
-    if (g_variant == 5 && aligned16(A)) {
-      if constexpr (LX == 8) return launch_row<LX, FAST>(A, nel, st, hx, hxt);
-    }
   }
   if constexpr (LX <= 12) {
-    if ((g_variant >= 3 || g_variant == 0) && aligned16(A)) {
+    if ((g_variant >= 4 || g_variant == 0) && aligned16(A)) {
       if constexpr (LX == 8) {
         if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
         if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
