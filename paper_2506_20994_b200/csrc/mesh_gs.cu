@@ -264,30 +264,53 @@ __device__ __forceinline__ void node_elems(int64_t g, int n1, int64_t lo, int64_
 // Walks the copies of node (gx, gy, gz) in ascending local order: OP 0 sums
 // and writes back (skipping unshared nodes), 1 = PARTIAL (sum -> buf),
 // 2 = FINISH (continue from buf, write back, sum -> buf), 3 = WRITE (buf -> copies).
+// Copies of node (gx, gy, gz): along each axis the node lies in one element,
+// or in two when it sits on an interior element face.  The first copy's flat
+// offset is computed once; the others differ by compile-time strides
+// (next element in x: +L3 - n1, in y: +nx L3 - n1 LX, in z: +nx ny L3 - n1 LX^2).
+template <int LX>
+__device__ __forceinline__ void gs_box_copies(const BoxGS& M, int gx, int gy, int gz, int64_t& off0,
+                                              int& cx, int& cy, int& cz, int64_t& DY, int64_t& DZ) {
+  constexpr int n1 = LX - 1;
+  constexpr int L3 = LX * LX * LX;
+  const int qx = gx / n1, rx = gx - qx * n1;
+  const int qy = gy / n1, ry = gy - qy * n1;
+  const int qz = gz / n1, rz = gz - qz * n1;
+  int ex0 = (rx == 0) ? qx - 1 : qx, ey0 = (ry == 0) ? qy - 1 : qy, ez0 = (rz == 0) ? qz - 1 : qz;
+  int ex1 = min(qx, M.nx - 1), ey1 = min(qy, M.ny - 1), ez1 = min(qz, (int)M.ez1 - 1);
+  ex0 = max(ex0, 0);
+  ey0 = max(ey0, 0);
+  ez0 = max(ez0, (int)M.ez0);
+  cx = ex1 - ex0 + 1;
+  cy = ey1 - ey0 + 1;
+  cz = ez1 - ez0 + 1;
+  const int64_t e = ((int64_t)(ez0 - M.ez0) * M.ny + ey0) * M.nx + ex0;
+  off0 = e * L3 + ((gz - ez0 * n1) * LX + (gy - ey0 * n1)) * LX + (gx - ex0 * n1);
+  DY = (int64_t)M.nx * L3 - n1 * LX;
+  DZ = (int64_t)M.nx * M.ny * L3 - n1 * LX * LX;
+}
+
+// Walks the copies of node (gx, gy, gz) in ascending local order: OP 0 sums
+// and writes back (skipping unshared nodes), 1 = PARTIAL (sum -> buf),
+// 2 = FINISH (continue from buf, write back, sum -> buf), 3 = WRITE (buf -> copies).
 template <int LX, int OP>
 __device__ __forceinline__ void gs_box_node(double* __restrict__ w, const BoxGS& M, int gx, int gy,
                                             int gz, double* __restrict__ buf) {
   constexpr int n1 = LX - 1;
   constexpr int L3 = LX * LX * LX;
-  // each axis contributes one or two elements (a node on an element face)
-  const int x0 = max((gx % n1 == 0) ? gx / n1 - 1 : gx / n1, 0), x1 = min(gx / n1, M.nx - 1);
-  const int y0 = max((gy % n1 == 0) ? gy / n1 - 1 : gy / n1, 0), y1 = min(gy / n1, M.ny - 1);
-  const int z0 = max((gz % n1 == 0) ? gz / n1 - 1 : gz / n1, (int)M.ez0);
-  const int z1 = min(gz / n1, (int)M.ez1 - 1);
-  const int cx = x1 - x0 + 1, cy = y1 - y0 + 1, cz = z1 - z0 + 1;  // 1 or 2 each
+  constexpr int64_t DX = L3 - n1;
+  int64_t off0, DY, DZ;
+  int cx, cy, cz;
+  gs_box_copies<LX>(M, gx, gy, gz, off0, cx, cy, cz, DY, DZ);
   if (OP == 0 && cx * cy * cz < 2) return;
   const int64_t slot = (int64_t)gy * M.NX + gx;
-  // flat offsets of the (up to 8) copies, ascending (ez, ey, ex) = ascending local index
-  int64_t off[8];
   bool ok[8];
+  int64_t off[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
+  for (int c = 0; c < 8; ++c) {  // c = (dz, dy, dx): ascending (ez, ey, ex)
     const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
     ok[c] = dz < cz && dy < cy && dx < cx;
-    const int ez = z0 + dz, ey = y0 + dy, ex = x0 + dx;
-    const int64_t e = ((int64_t)(ez - M.ez0) * M.ny + ey) * M.nx + ex;
-    const int p = ((gz - ez * n1) * LX + (gy - ey * n1)) * LX + (gx - ex * n1);
-    off[c] = e * L3 + p;
+    off[c] = off0 + dx * DX + dy * DY + dz * DZ;
   }
   double s = (OP == 2 || OP == 3) ? buf[slot] : 0.0;
   if (OP != 3) {
@@ -322,33 +345,86 @@ __global__ void gs_box_plane_kernel(double* __restrict__ w, const BoxGS M, int g
 //  CLS 1: the other planes, rows on y faces (gy % n1 == 0): every gx
 //  CLS 2: the other planes and rows: x-face nodes only (gx = fx * n1)
 // z-plane sets are [zlo, zhi] (inclusive) of node planes owned locally.
-template <int LX, int CLS>
-__global__ void gs_box_local_kernel(double* __restrict__ w, const BoxGS M, int zlo, int zhi, int qlo) {
+// CLS 0 / 1 threads take NB nodes (consecutive rows / planes) and issue all
+// their loads before any sum (the one-node version was latency-bound at
+// 2-3 TB/s: only 2-4 independent loads per thread); CLS 2 is already
+// sector-bound and stays one node per thread.
+template <int LX, int NB>
+__device__ __forceinline__ void gs_box_local_nodes(double* __restrict__ w, const BoxGS& M,
+                                                   const int (&gx)[NB], const int (&gy)[NB],
+                                                   const int (&gz)[NB], const bool (&use)[NB]) {
   constexpr int n1 = LX - 1;
-  int gz, gy, gx;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (CLS == 0) {
-    gz = ((zlo + n1 - 1) / n1 + (int)blockIdx.z) * n1;  // face planes in [zlo, zhi]
-    gy = blockIdx.y;
-    gx = t;
-    if (gx >= M.NX) return;
-  } else {
-    // the q-th non-face node plane overall is (q/(n1-1))*n1 + 1 + q%(n1-1)
-    const int q = qlo + (int)blockIdx.z;
-    gz = (q / (n1 - 1)) * n1 + 1 + q % (n1 - 1);
-    if (CLS == 1) {
-      gy = (int)blockIdx.y * n1;
-      gx = t;
-      if (gx >= M.NX) return;
-    } else {
-      const int r = blockIdx.y;  // non-face row index
-      gy = (r / (n1 - 1)) * n1 + 1 + r % (n1 - 1);
-      gx = (t + 1) * n1;  // interior x faces fx = 1 .. nx-1
-      if (t >= M.nx - 1) return;
+  constexpr int L3 = LX * LX * LX;
+  constexpr int64_t DX = L3 - n1;
+  int64_t off[NB][8];
+  bool ok[NB][8];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    int64_t off0, DY, DZ;
+    int cx, cy, cz;
+    gs_box_copies<LX>(M, gx[b], gy[b], gz[b], off0, cx, cy, cz, DY, DZ);
+    const bool shared = use[b] && cx * cy * cz >= 2;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+      ok[b][c] = shared && dz < cz && dy < cy && dx < cx;
+      off[b][c] = off0 + dx * DX + dy * DY + dz * DZ;
     }
   }
-  if (gz > zhi) return;
-  gs_box_node<LX, 0>(w, M, gx, gy, gz, nullptr);
+  double v[NB][8];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[b][c] = ok[b][c] ? w[off[b][c]] : 0.0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (ok[b][c]) s = __dadd_rn(s, v[b][c]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (ok[b][c]) w[off[b][c]] = s;
+  }
+}
+
+template <int CLS>
+struct GsNB {
+  static constexpr int NB = 1;
+};
+
+template <int LX, int CLS>
+__global__ void gs_box_local_kernel(double* __restrict__ w, const BoxGS M, int zlo, int zhi, int qlo,
+                                    int nrows) {
+  constexpr int n1 = LX - 1;
+  constexpr int NB = GsNB<CLS>::NB;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int gx[NB], gy[NB], gz[NB];
+  bool use[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int rb = (int)blockIdx.y * NB + b;  // batched index
+    if (CLS == 0) {
+      gz[b] = ((zlo + n1 - 1) / n1 + (int)blockIdx.z) * n1;
+      gy[b] = rb;
+      gx[b] = t;
+      use[b] = gx[b] < M.NX && rb < nrows && gz[b] <= zhi;
+    } else if (CLS == 1) {
+      const int q = qlo + rb;  // the rb-th non-face plane of the range
+      gz[b] = (q / (n1 - 1)) * n1 + 1 + q % (n1 - 1);
+      gy[b] = (int)blockIdx.z * n1;
+      gx[b] = t;
+      use[b] = gx[b] < M.NX && rb < nrows && gz[b] <= zhi;
+    } else {
+      const int q = qlo + (int)blockIdx.z;
+      gz[b] = (q / (n1 - 1)) * n1 + 1 + q % (n1 - 1);
+      gy[b] = (rb / (n1 - 1)) * n1 + 1 + rb % (n1 - 1);
+      gx[b] = (t + 1) * n1;
+      use[b] = t < M.nx - 1 && rb < nrows && gz[b] <= zhi;
+    }
+    if (!use[b]) gx[b] = gy[b] = gz[b] = n1;  // any in-range node; not touched
+  }
+  gs_box_local_nodes<LX, NB>(w, M, gx, gy, gz, use);
 }
 
 template <int LX>
@@ -364,21 +440,23 @@ static cudaError_t gs_box_launch(int op, double* w, const BoxGS& M, int has_belo
       if (hi < lo) break;
       // face planes in [lo, hi]
       const int f0 = (lo + n1 - 1) / n1, f1 = hi / n1;
-      if (f1 >= f0)
-        gs_box_local_kernel<LX, 0><<<dim3(gxb, (unsigned)M.NY, (unsigned)(f1 - f0 + 1)), blk, 0, st>>>(
-            w, M, lo, hi, 0);
+      const auto nb = [](int64_t rows, int NB) { return (unsigned)((rows + NB - 1) / NB); };
+      if (f1 >= f0)  // y: rows gy (batched), z: face planes
+        gs_box_local_kernel<LX, 0><<<dim3(gxb, nb(M.NY, GsNB<0>::NB), (unsigned)(f1 - f0 + 1)), blk, 0,
+                                     st>>>(w, M, lo, hi, 0, (int)M.NY);
       if (n1 > 1) {
         // non-face planes in [lo, hi]
         const int nnf = (hi - lo + 1) - (f1 >= f0 ? f1 - f0 + 1 : 0);
         const int lo2 = (lo % n1 == 0) ? lo + 1 : lo;
         const int qlo = (lo2 / n1) * (n1 - 1) + (lo2 % n1 - 1);
         if (nnf > 0) {
-          gs_box_local_kernel<LX, 1><<<dim3(gxb, (unsigned)(M.ny + 1), (unsigned)nnf), blk, 0, st>>>(
-              w, M, lo, hi, qlo);
-          if (M.nx > 1)
+          // y: non-face planes (batched), z: y-face rows
+          gs_box_local_kernel<LX, 1><<<dim3(gxb, nb(nnf, GsNB<1>::NB), (unsigned)(M.ny + 1)), blk, 0,
+                                       st>>>(w, M, lo, hi, qlo, nnf);
+          if (M.nx > 1)  // y: non-face rows, z: non-face planes
             gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
-                                              (unsigned)(M.ny * (n1 - 1)), (unsigned)nnf),
-                                         blk, 0, st>>>(w, M, lo, hi, qlo);
+                                              nb((int64_t)M.ny * (n1 - 1), GsNB<2>::NB), (unsigned)nnf),
+                                         blk, 0, st>>>(w, M, lo, hi, qlo, M.ny * (n1 - 1));
         }
       }
       break;
