@@ -329,7 +329,8 @@ def ours_arm(args):
     nx, ny, nzr = mesh_dims(nel)
     mesh = BoxMesh(nx, ny, nzr * ws, lx, rank, ws)
     assert mesh.nel == nel
-    op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1)
+    op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1,
+                           schedule=args.gs_schedule if not args.gs_schedule.isdigit() else int(args.gs_schedule))
     g = torch.Generator(device=device).manual_seed(1234 + rank)
     u = torch.randn(mesh.shape, dtype=torch.float64, device=device, generator=g)
     w = torch.empty_like(u)
@@ -416,11 +417,19 @@ def ours_arm(args):
     if not args.no_gs:
         g_total, _, _ = timed_fn(lambda: op.apply(u, w), args.gs_steps, 3, False)
         g_ms = g_total / args.gs_steps
+        # the concurrent-follower schedule for comparison (DSSUM on w in L2)
+        op0 = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, geometry=op.geom,
+                                schedule="follow")
+        u0_total, _, _ = timed_fn(lambda: op0.apply(u, w), args.gs_steps, 3, False)
+        u0_ms = u0_total / args.gs_steps
+        del op0
         gs_line = {"workload": f"w = QQ^T A u on a {mesh.nx}x{mesh.ny}x{mesh.nz} brick "
                                f"(z-slab of {mesh.ez1 - mesh.ez0} layers per rank), lx={lx}",
                    "steps": args.gs_steps, "ms_per_step": round(g_ms, 5),
                    "gdof_s": round(pts * ws / (g_ms * 1e-3) / 1e9, 4),
                    "dssum_ms": round(g_ms - total_ms / args.steps, 5),
+                   "schedule": {-1: "follow", 0: "sequential"}.get(op.schedule, op.schedule),
+                   "follow_schedule_ms_per_step": round(u0_ms, 5),
                    "exchange": ("NCCL P2P planes, overlapped with interior ax" if ws > 1 and not
                                 comm.host_staged else ("gloo host-staged planes" if ws > 1 else "none (1 rank)")),
                    "plane_bytes": mesh.plane * 8}
@@ -571,6 +580,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gs", action="store_true", help="skip the ax + DSSUM measurement")
     ap.add_argument("--gs-steps", type=int, default=50)
+    ap.add_argument("--gs-schedule", default="sequential",
+                    help="ax + DSSUM schedule: follow | sequential | <layers per block>")
     ap.add_argument("--no-cg", action="store_true", help="skip the Jacobi-PCG measurement")
     ap.add_argument("--cg-iters", type=int, default=100)
     ap.add_argument("--cpu-nel", type=int, default=CPU_SAMPLE_NEL)

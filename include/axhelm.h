@@ -35,6 +35,11 @@ extern "C" {
 #endif
 
 enum axhelm_mode { AXHELM_STRICT = 0, AXHELM_FAST = 1 };
+/* Flag OR-ed into the mode of axhelm_apply / axhelm_apply_dot: the caller
+ * reads w again right after the apply (layer-blocked ax + DSSUM), so the
+ * kernel loads its inputs L2 evict-first and keeps w in L2 instead of
+ * streaming it out.  Results are identical with or without it. */
+enum { AXHELM_KEEP_W_L2 = 0x100 };
 
 enum axhelm_status {
   AXHELM_OK = 0,
@@ -133,6 +138,41 @@ int axhelm_gs_plane(int op, double* w, const int64_t* offs, const void* idx, int
  * Same summation order as axhelm_gs_sum. */
 int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
                   int has_below, int has_above, double* buf, void* stream);
+
+/* Local DSSUM (op 0 of axhelm_gs_box) restricted to the global z node planes
+ * [zlo, zhi] of the slab, which must not include an exchanged interface
+ * plane.  Summing the planes in ascending blocks gives the same result as
+ * one op-0 call; a caller interleaves it with ax_helm on element layers so
+ * the w it touches is still in L2. */
+int axhelm_gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                        int64_t zlo, int64_t zhi, void* stream);
+
+/* Assembled local operator on a BoxMesh slab: ax_helm on the slab's local
+ * element layers [l0, l1) and the local DSSUM of the owned node planes
+ * [zlo, zhi] (layers outside [l0, l1) must already be applied, stream-
+ * ordered before this call).  The 15 pointers are the slab's arrays
+ * (element 0 = first element of layer ez0).  schedule:
+ *   AXHELM_SCHED_SEQUENTIAL (0): one apply streaming w to HBM, then one
+ *       DSSUM pass (reads and writes w again);
+ *   AXHELM_SCHED_FOLLOW (-1): the apply keeps w in L2 and publishes per-layer
+ *       completion counters in progress[l1 - l0] (zeroed here); a DSSUM
+ *       follower kernel runs concurrently on an internal stream (joined back
+ *       into `stream`) and sums each layer's planes as soon as it is
+ *       complete (TMA-ring kernels, lx <= 12; else sequential);
+ *   n > 0: blocks of n layers, each apply followed by the DSSUM of the planes
+ *       it completes (kernel-boundary version of FOLLOW).
+ * dot_out (nullable): sum_p u_p (A u)_p over the applied elements before
+ * assembly (fixed order); partial then needs axhelm_ax_gs_scratch(l1 - l0)
+ * doubles.  Every schedule gives bit-identical w. */
+enum { AXHELM_SCHED_SEQUENTIAL = 0, AXHELM_SCHED_FOLLOW = -1 };
+int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int nx, int ny,
+                     int lx, int64_t ez0, int64_t ez1, int64_t l0, int64_t l1, int64_t zlo,
+                     int64_t zhi, int mode, int schedule, unsigned* progress, double* partial,
+                     double* dot_out, void* stream);
+int axhelm_ax_gs_scratch(int64_t nlayers);
 
 /* ---- Jacobi-PCG building blocks (no reference) --------
  * Deterministic reductions: `partial` holds axhelm_reduce_blocks(n) * 2

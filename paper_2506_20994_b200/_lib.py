@@ -33,7 +33,12 @@ PROTOTYPES = {
                                        _vp, _vp]),
     "axhelm_gs_box": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp]),
+    "axhelm_gs_box_range": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp]),
     "axhelm_reduce_blocks": (ctypes.c_int, [ctypes.c_int64]),
+    "axhelm_ax_gs_box": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int] * 3 + [ctypes.c_int64] * 6
+                         + [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "axhelm_ax_gs_scratch": (ctypes.c_int, [ctypes.c_int64]),
     "axhelm_dot": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "axhelm_cg_init": (ctypes.c_int, [_vp] * 7 + [ctypes.c_int64, _vp, _vp, _vp]),
     "axhelm_cg_update": (ctypes.c_int, [_vp] * 7 + [ctypes.c_int64, _vp, _vp, _vp]),

@@ -73,6 +73,7 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
   const int lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int64_t stride = gridDim.x;
+  const L2Pol pol = make_l2pol(A.keep_w);
 
   if (tid == 0) {
     for (int d = 0; d < C::D; ++d) mbar_init(&bars[d], 1);
@@ -82,7 +83,7 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
   if (tid == 0)
     for (int d = 0; d < C::D; ++d) {
       const int64_t e = blockIdx.x + d * stride;
-      if (e < nel) issue_group<8>(A, nel, e, bufs + d * C::BUF, &bars[d]);
+      if (e < nel) issue_group<8>(A, nel, e, bufs + d * C::BUF, &bars[d], pol.in);
     }
 
   // matrix fragments, fixed for the whole CTA
@@ -214,16 +215,16 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
       const int o = k * 64 + g * 8 + 2 * q;
       const double2 z = lds2(ST + o);
       const double w0 = w[kt][0] + z.x, w1 = w[kt][1] + z.y;
-      asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(wout + o), "d"(w0), "d"(w1)
-                   : "memory");
+      stg_w2(wout + o, w0, w1, pol);
       if constexpr (DOT) dot_acc = fma(uown[kt][0], w0, fma(uown[kt][1], w1, dot_acc));
     }
     __syncthreads();  // buffer b and ST free
     if (tid == 0) {
+      if (A.progress) signal_done(A, e, 1);
       const int64_t en = e + C::D * stride;
       if (en < nel) {
         fence_proxy_async();
-        issue_group<8>(A, nel, en, buf, &bars[b]);
+        issue_group<8>(A, nel, en, buf, &bars[b], pol.in);
       }
     }
   }

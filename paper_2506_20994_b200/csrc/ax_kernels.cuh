@@ -50,7 +50,30 @@ struct AxPtrs {
   const double* __restrict__ g12;
   const double* __restrict__ g13;
   const double* __restrict__ g23;
+  // 1: the caller reads w again soon (layer-blocked ax + DSSUM): inputs are
+  // loaded L2 evict-first and w is stored evict-normal so it stays in L2;
+  // 0 (default): w is streamed out evict-first.
+  int keep_w = 0;
+  // optional completion counters for a concurrent consumer (the DSSUM
+  // follower, mesh_gs.cu): after an element's w is stored, progress[e / lay]
+  // is incremented with release semantics at gpu scope
+  unsigned* progress = nullptr;
+  int64_t lay = 0;
 };
+
+// Thread 0, after a __syncthreads that follows every thread's w stores of
+// elements [e0, e0 + ne): publish them (the CUTLASS semaphore pattern: the
+// barrier orders the CTA's stores before thread 0's release).
+__device__ __forceinline__ void signal_done(const AxPtrs& A, int64_t e0, int64_t ne) {
+  const int64_t end = e0 + ne;
+  for (int64_t e = e0; e < end;) {
+    const int64_t L = e / A.lay;
+    const int64_t stop = (L + 1) * A.lay < end ? (L + 1) * A.lay : end;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(A.progress + L), "r"((unsigned)(stop - e))
+                 : "memory");
+    e = stop;
+  }
+}
 
 template <int LX>
 struct KCfg {
@@ -95,6 +118,38 @@ __device__ __forceinline__ double ldg_stream(const double* p) {
 
 __device__ __forceinline__ void stg_stream(double* p, double v) {
   asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// L2 cache policies (createpolicy): the TMA input stream and the w stores.
+struct L2Pol {
+  uint64_t in, w;
+  bool keep;
+};
+__device__ __forceinline__ L2Pol make_l2pol(int keep_w) {
+  L2Pol P;
+  P.keep = keep_w != 0;
+  if (P.keep) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(P.in));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(P.w));
+  } else {
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(P.in));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(P.w));
+  }
+  return P;
+}
+// w store: streamed (evict-first) unless the policy keeps w in L2
+__device__ __forceinline__ void stg_w(double* p, double v, const L2Pol& P) {
+  if (P.keep)
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(P.w) : "memory");
+  else
+    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void stg_w2(double* p, double v0, double v1, const L2Pol& P) {
+  if (P.keep)
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v0), "d"(v1), "l"(P.w)
+                 : "memory");
+  else
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v0), "d"(v1) : "memory");
 }
 
 // v1 k-walk kernel: one CTA per EPB elements.

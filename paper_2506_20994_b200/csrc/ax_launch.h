@@ -23,6 +23,9 @@ cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream
 // fused lx = 8 fast apply + per-CTA partials of sum u*w (nparts written)
 cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int* nparts,
                              cudaStream_t st);
+// true when launch_ax would run a kernel that honours AxPtrs::progress
+// (the TMA-ring kernels: lx <= 12, 16-B aligned fields)
+bool progress_capable(const AxPtrs& A, int lx);
 // true when launch_ax would run the fused-capable DMMA kernel
 bool dmma8_selected(const AxPtrs& A, int lx, int mode);
 
@@ -30,5 +33,19 @@ bool dmma8_selected(const AxPtrs& A, int lx, int mode);
 // pageable host) and run the apply synchronously, staging host data through
 // the GPU in copy/compute-overlapped chunks.
 int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int mode);
+
+// structured DSSUM of the slab's node planes [zlo, zhi] (mesh_gs.cu);
+// gs_box_range_check returns nullptr or why the arguments are invalid
+cudaError_t gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                         int64_t zhi, cudaStream_t st);
+const char* gs_box_range_check(int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                               int64_t zhi);
+
+// DSSUM follower: the local DSSUM of node planes [zlo, zhi] of local layers
+// [0, nl), run CONCURRENTLY with an apply over layers [l0, l1) that signals
+// per-layer completion in progress[L - l0] (layers outside [l0, l1) must be
+// complete already).  Each layer's planes are summed once the layer is done.
+cudaError_t gs_box_follow(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                          int64_t zhi, const unsigned* progress, int64_t l0, int64_t l1, cudaStream_t st);
 
 }  // namespace axb

@@ -84,6 +84,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -106,7 +115,7 @@ __device__ __forceinline__ const double* field_ptr(const AxPtrs& A, int f) {
 // Returns true when the bulk path was used.
 template <int LX>
 __device__ __forceinline__ bool issue_group(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
-                                            uint64_t* bar) {
+                                            uint64_t* bar, uint64_t pol) {
   using C = TCfg<LX>;
   const int64_t e0 = g * C::EPL;
   const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
@@ -117,7 +126,7 @@ __device__ __forceinline__ bool issue_group(const AxPtrs& A, int64_t nel, int64_
   }
   mbar_arrive_expect_tx(bar, 8u * bytes);
 #pragma unroll
-  for (int f = 0; f < 8; ++f) bulk_g2s(buf + f * C::FIELD, field_ptr(A, f) + e0 * C::L3, bytes, bar);
+  for (int f = 0; f < 8; ++f) bulk_g2s_hint(buf + f * C::FIELD, field_ptr(A, f) + e0 * C::L3, bytes, bar, pol);
   return true;
 }
 
@@ -157,6 +166,7 @@ ax_stream_probe(const AxPtrs A, const int64_t nel) {
   const int tid = threadIdx.x;
   const int64_t ngroups = (nel + C::EPL - 1) / C::EPL;
   const int64_t stride = gridDim.x;
+  const L2Pol pol = make_l2pol(0);
   if (tid == 0) {
     for (int d = 0; d < C::D; ++d) mbar_init(&bars[d], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -165,7 +175,7 @@ ax_stream_probe(const AxPtrs A, const int64_t nel) {
   if (tid == 0)
     for (int d = 0; d < C::D; ++d) {
       const int64_t g = blockIdx.x + d * stride;
-      if (g < ngroups) issue_group<LX>(A, nel, g, bufs + d * C::BUF, &bars[d]);
+      if (g < ngroups) issue_group<LX>(A, nel, g, bufs + d * C::BUF, &bars[d], pol.in);
     }
   int64_t n = 0;
   for (int64_t g = blockIdx.x; g < ngroups; g += stride, ++n) {
@@ -185,7 +195,7 @@ ax_stream_probe(const AxPtrs A, const int64_t nel) {
       const int64_t gn = g + C::D * stride;
       if (gn < ngroups) {
         fence_proxy_async();
-        issue_group<LX>(A, nel, gn, buf, &bars[b]);
+        issue_group<LX>(A, nel, gn, buf, &bars[b], pol.in);
       }
     }
   }

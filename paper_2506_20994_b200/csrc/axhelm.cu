@@ -230,6 +230,10 @@ static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+bool progress_capable(const AxPtrs& A, int lx) {
+  return lx <= 12 && (g_variant == 0 || g_variant == 4 || g_variant == 6) && aligned16(A);
+}
+
 bool dmma8_selected(const AxPtrs& A, int lx, int mode) {
   return lx == 8 && mode == AXHELM_FAST && (g_variant == 0 || g_variant == 6) && aligned16(A);
 }
@@ -346,6 +350,8 @@ int axhelm_apply(double* wd, const double* ud, const double* dxd, const double* 
                  int mode, void* stream) {
   if (lx < 2 || lx > 16) return set_status(AXHELM_EINVAL, "lx=%d outside [2, 16]", lx);
   if (nel < 0) return set_status(AXHELM_EINVAL, "nel=%lld is negative", (long long)nel);
+  const int keep = (mode & AXHELM_KEEP_W_L2) != 0;
+  mode &= ~AXHELM_KEEP_W_L2;
   if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
     return set_status(AXHELM_EINVAL, "unknown mode %d", mode);
   if (nel == 0) return set_status(AXHELM_OK, "");
@@ -353,7 +359,7 @@ int axhelm_apply(double* wd, const double* ud, const double* dxd, const double* 
                             h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   for (int q = 0; q < 15; ++q)
     if (!ptrs[q]) return set_status(AXHELM_EINVAL, "argument %d is NULL", q);
-  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d, keep};
   return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream), "axhelm_apply");
 }
 

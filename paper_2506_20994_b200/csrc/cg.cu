@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "../../include/axhelm.h"
 #include "ax_launch.h"
@@ -192,33 +193,167 @@ int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const doub
   return cuda_status(cudaGetLastError(), "axhelm_cg_pupdate");
 }
 
-int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const double* dyd,
-                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
-                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
-                     const double* g12d, const double* g13d, const double* g23d, int64_t nel,
-                     int lx, int mode, double* partial, double* out, void* stream) {
-  if (lx < 2 || lx > 16 || nel < 0) return set_status(AXHELM_EINVAL, "axhelm_apply_dot: bad sizes");
-  cudaStream_t st = (cudaStream_t)stream;
-  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+}  // extern "C"
+
+namespace axb {
+// ax_helm + out[0] = sum u*w over the nel elements (fused for the lx = 8
+// DMMA kernel, else a separate fixed-order dot pass); partial: block scratch
+static cudaError_t ax_dot(const AxPtrs& A, int64_t nel, int lx, int mode, double* partial, double* out,
+                          cudaStream_t st) {
   const int64_t n = nel * lx * lx * lx;
   cudaError_t e;
-  if (nel > 0 && dmma8_selected(A, lx, mode)) {
+  if (dmma8_selected(A, lx, mode)) {
     int nb = 0;
     e = launch_dmma8_dot(A, nel, partial, &nb, st);
     if (e == cudaSuccess) {
       reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
       e = cudaGetLastError();
     }
-    return cuda_status(e, "axhelm_apply_dot");
+    return e;
   }
   e = launch_ax(A, nel, lx, mode, st);
   if (e == cudaSuccess) {
     const int nb = red_blocks(n);
-    dot_kernel<<<nb, RT, 0, st>>>(ud, wd, nullptr, n, partial);
+    dot_kernel<<<nb, RT, 0, st>>>(A.u, A.w, nullptr, n, partial);
     reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
     e = cudaGetLastError();
   }
-  return cuda_status(e, "axhelm_apply_dot");
+  return e;
+}
+
+// the follower's stream and fork/join events, one set per device
+struct FollowStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static FollowStreams* follow_streams() {
+  static std::mutex mu;
+  static FollowStreams fs[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  FollowStreams& f = fs[dev];
+  if (!f.side) {
+    if (cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess) {
+      f.side = nullptr;
+      return nullptr;
+    }
+  }
+  return &f;
+}
+
+static int max_partials() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms * 8;  // >= red_blocks(n) and >= the DMMA grid
+}
+}  // namespace axb
+
+extern "C" {
+
+int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int64_t nel,
+                     int lx, int mode, double* partial, double* out, void* stream) {
+  if (lx < 2 || lx > 16 || nel < 0) return set_status(AXHELM_EINVAL, "axhelm_apply_dot: bad sizes");
+  const int keep = (mode & AXHELM_KEEP_W_L2) != 0;
+  mode &= ~AXHELM_KEEP_W_L2;
+  if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
+    return set_status(AXHELM_EINVAL, "axhelm_apply_dot: unknown mode %d", mode);
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d, keep};
+  if (nel == 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream);
+    return cuda_status(e, "axhelm_apply_dot");
+  }
+  return cuda_status(ax_dot(A, nel, lx, mode, partial, out, (cudaStream_t)stream), "axhelm_apply_dot");
+}
+
+int axhelm_ax_gs_scratch(int64_t nlayers) { return max_partials() + (int)(nlayers > 0 ? nlayers : 0); }
+
+int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int nx, int ny,
+                     int lx, int64_t ez0, int64_t ez1, int64_t l0, int64_t l1, int64_t zlo,
+                     int64_t zhi, int mode, int schedule, unsigned* progress, double* partial,
+                     double* dot_out, void* stream) {
+  const int64_t nl = ez1 - ez0;
+  if (const char* why = gs_box_range_check(nx, ny, lx, ez0, ez1, zlo, zhi))
+    return set_status(AXHELM_EINVAL, "axhelm_ax_gs_box: %s", why);
+  if (l0 < 0 || l1 > nl || l1 < l0) return set_status(AXHELM_EINVAL, "axhelm_ax_gs_box: bad layer range");
+  if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
+    return set_status(AXHELM_EINVAL, "axhelm_ax_gs_box: unknown mode %d", mode);
+  if (dot_out && !partial) return set_status(AXHELM_EINVAL, "axhelm_ax_gs_box: dot needs partial scratch");
+  if (schedule == AXHELM_SCHED_FOLLOW && !progress)
+    return set_status(AXHELM_EINVAL, "axhelm_ax_gs_box: the follow schedule needs progress scratch");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n1 = lx - 1;
+  const int64_t L3 = (int64_t)lx * lx * lx, lay = (int64_t)nx * ny;
+  const int pmax = max_partials();
+  double* chunk_dot = partial ? partial + pmax : nullptr;
+  auto ptrs_at = [&](int64_t layer, int keep) {
+    const int64_t o = layer * lay * L3;
+    return AxPtrs{wd + o, ud + o, dxd, dyd, dzd, dxtd, dytd, dztd, h1d + o, g11d + o, g22d + o, g33d + o,
+                  g12d + o, g13d + o, g23d + o, keep};
+  };
+  cudaError_t e = cudaSuccess;
+  if (schedule == AXHELM_SCHED_FOLLOW) {
+    AxPtrs A = ptrs_at(l0, 1);
+    A.progress = progress;
+    A.lay = lay;
+    // the dot of the non-fused kernels is a separate pass over w, which the
+    // follower is already assembling: those run the sequential schedule
+    if (l1 > l0 && progress_capable(A, lx) && (!dot_out || dmma8_selected(A, lx, mode))) {
+      FollowStreams* fs = follow_streams();
+      if (!fs) return set_status(AXHELM_ECUDA, "axhelm_ax_gs_box: cannot create the follower stream");
+      // The apply is enqueued first and never waits on the follower, so it
+      // always completes; the follower only waits on the apply's counters.
+      // Its CTAs are small (128 threads, <= 64 registers, no shared memory)
+      // and fit beside the apply's persistent CTAs on the same SMs.
+      e = cudaMemsetAsync(progress, 0, sizeof(unsigned) * (size_t)(l1 - l0), st);
+      if (e == cudaSuccess) e = cudaEventRecord(fs->fork, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(fs->side, fs->fork, 0);
+      if (e == cudaSuccess)
+        e = dot_out ? ax_dot(A, (l1 - l0) * lay, lx, mode, partial, dot_out, st)
+                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st);
+      if (e == cudaSuccess) e = gs_box_follow(wd, nx, ny, lx, ez0, ez1, zlo, zhi, progress, l0, l1, fs->side);
+      if (e == cudaSuccess) e = cudaEventRecord(fs->join, fs->side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, fs->join, 0);
+      return cuda_status(e, "axhelm_ax_gs_box");
+    }
+    schedule = AXHELM_SCHED_SEQUENTIAL;
+  }
+  const int64_t B = schedule > 0 ? schedule : (l1 - l0 > 0 ? l1 - l0 : 1);
+  int64_t next = zlo;  // first plane not yet summed
+  int nchunks = 0;
+  for (int64_t a = l0; a < l1 && e == cudaSuccess; a += B, ++nchunks) {
+    const int64_t b = (a + B < l1) ? a + B : l1;
+    AxPtrs A = ptrs_at(a, schedule > 0 ? 1 : 0);
+    const int64_t nel = (b - a) * lay;
+    e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st) : launch_ax(A, nel, lx, mode, st);
+    if (e != cudaSuccess) break;
+    // planes whose every copy is computed: below layer ez0 + b, or all when
+    // the layers above l1 are done by the caller
+    const int64_t top = (b == l1) ? zhi : ((ez0 + b) * n1 - 1 < zhi ? (ez0 + b) * n1 - 1 : zhi);
+    if (top >= next) {
+      e = gs_box_range(wd, nx, ny, lx, ez0, ez1, next, top, st);
+      next = top + 1;
+    }
+  }
+  if (e == cudaSuccess && next <= zhi) e = gs_box_range(wd, nx, ny, lx, ez0, ez1, next, zhi, st);
+  if (e == cudaSuccess && dot_out) {
+    if (nchunks == 0) {
+      e = cudaMemsetAsync(dot_out, 0, sizeof(double), st);
+    } else {
+      reduce_partials_kernel<<<1, RT, 0, st>>>(chunk_dot, nchunks, 1, dot_out);
+      e = cudaGetLastError();
+    }
+  }
+  return cuda_status(e, "axhelm_ax_gs_box");
 }
 
 int axhelm_diag(double* diag, const double* dxd, const double* dyd, const double* dzd,

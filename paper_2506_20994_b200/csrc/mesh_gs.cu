@@ -427,6 +427,38 @@ __global__ void gs_box_local_kernel(double* __restrict__ w, const BoxGS M, int z
   gs_box_local_nodes<LX, NB>(w, M, gx, gy, gz, use);
 }
 
+// Local DSSUM of the owned node planes [lo, hi] (global z node-plane
+// indices; every copy of those nodes lies in the slab): three launches, one
+// per node class.
+template <int LX>
+static void gs_box_local_range(double* w, const BoxGS& M, int lo, int hi, cudaStream_t st) {
+  constexpr int n1 = LX - 1;
+  if (hi < lo) return;
+  const dim3 blk(128);
+  const unsigned gxb = (unsigned)((M.NX + 127) / 128);
+  // face planes in [lo, hi]
+  const int f0 = (lo + n1 - 1) / n1, f1 = hi / n1;
+  const auto nb = [](int64_t rows, int NB) { return (unsigned)((rows + NB - 1) / NB); };
+  if (f1 >= f0)  // y: rows gy (batched), z: face planes
+    gs_box_local_kernel<LX, 0><<<dim3(gxb, nb(M.NY, GsNB<0>::NB), (unsigned)(f1 - f0 + 1)), blk, 0,
+                                 st>>>(w, M, lo, hi, 0, (int)M.NY);
+  if (n1 > 1) {
+    // non-face planes in [lo, hi]
+    const int nnf = (hi - lo + 1) - (f1 >= f0 ? f1 - f0 + 1 : 0);
+    const int lo2 = (lo % n1 == 0) ? lo + 1 : lo;
+    const int qlo = (lo2 / n1) * (n1 - 1) + (lo2 % n1 - 1);
+    if (nnf > 0) {
+      // y: non-face planes (batched), z: y-face rows
+      gs_box_local_kernel<LX, 1><<<dim3(gxb, nb(nnf, GsNB<1>::NB), (unsigned)(M.ny + 1)), blk, 0,
+                                   st>>>(w, M, lo, hi, qlo, nnf);
+      if (M.nx > 1)  // y: non-face rows, z: non-face planes
+        gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
+                                          nb((int64_t)M.ny * (n1 - 1), GsNB<2>::NB), (unsigned)nnf),
+                                     blk, 0, st>>>(w, M, lo, hi, qlo, M.ny * (n1 - 1));
+    }
+  }
+}
+
 template <int LX>
 static cudaError_t gs_box_launch(int op, double* w, const BoxGS& M, int has_below, int has_above,
                                  double* buf, cudaStream_t st) {
@@ -437,28 +469,7 @@ static cudaError_t gs_box_launch(int op, double* w, const BoxGS& M, int has_belo
     case 0: {
       const int lo = (int)(M.ez0 * n1 + (has_below ? 1 : 0));
       const int hi = (int)(M.ez1 * n1 - (has_above ? 1 : 0));
-      if (hi < lo) break;
-      // face planes in [lo, hi]
-      const int f0 = (lo + n1 - 1) / n1, f1 = hi / n1;
-      const auto nb = [](int64_t rows, int NB) { return (unsigned)((rows + NB - 1) / NB); };
-      if (f1 >= f0)  // y: rows gy (batched), z: face planes
-        gs_box_local_kernel<LX, 0><<<dim3(gxb, nb(M.NY, GsNB<0>::NB), (unsigned)(f1 - f0 + 1)), blk, 0,
-                                     st>>>(w, M, lo, hi, 0, (int)M.NY);
-      if (n1 > 1) {
-        // non-face planes in [lo, hi]
-        const int nnf = (hi - lo + 1) - (f1 >= f0 ? f1 - f0 + 1 : 0);
-        const int lo2 = (lo % n1 == 0) ? lo + 1 : lo;
-        const int qlo = (lo2 / n1) * (n1 - 1) + (lo2 % n1 - 1);
-        if (nnf > 0) {
-          // y: non-face planes (batched), z: y-face rows
-          gs_box_local_kernel<LX, 1><<<dim3(gxb, nb(nnf, GsNB<1>::NB), (unsigned)(M.ny + 1)), blk, 0,
-                                       st>>>(w, M, lo, hi, qlo, nnf);
-          if (M.nx > 1)  // y: non-face rows, z: non-face planes
-            gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
-                                              nb((int64_t)M.ny * (n1 - 1), GsNB<2>::NB), (unsigned)nnf),
-                                         blk, 0, st>>>(w, M, lo, hi, qlo, M.ny * (n1 - 1));
-        }
-      }
+      gs_box_local_range<LX>(w, M, lo, hi, st);
       break;
     }
     case 1 + AXHELM_GS_PARTIAL:
@@ -501,4 +512,230 @@ extern "C" int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t 
       e = cudaErrorInvalidValue;
   }
   return cuda_status(e, "axhelm_gs_box");
+}
+
+namespace axb {
+// ------------------------------------------------------------------ follower
+// The local DSSUM as a consumer running concurrently with the ax_helm
+// kernel (on another stream): the apply publishes per-layer completion
+// counters (signal_done, release); one persistent CTA per SM walks the
+// slab's layers in order, waits (acquire) until layer L is complete, then
+// sums the node planes of layer L — the face plane below it and its
+// interior planes (the top plane too for the last layer) — while that w is
+// still in L2 (the apply stores w evict-normal and streams its inputs
+// evict-first).  Per node the copies are visited in the same ascending order
+// as gs_box_node, so the result is bit-identical to the separate pass.
+struct FollowArgs {
+  double* w;
+  BoxGS M;
+  const unsigned* progress;
+  int64_t l0, l1, lay;
+  int zlo, zhi;
+};
+
+__device__ __forceinline__ bool layer_complete(const FollowArgs& F, int64_t L) {
+  if (L < F.l0 || L >= F.l1) return true;
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(F.progress + (L - F.l0)) : "memory");
+  return (int64_t)v >= F.lay;
+}
+
+// timing trace of the last follower launch (CTA 0): [0] start, [1 + L] the
+// time layer L became available, [nl + 1] end — debug/profiling only
+__device__ unsigned long long g_follow_trace[1024];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One thread per node column (gx, gy) of the layer (grid-stride): the node
+// on the face plane below layer L (copies in layers L-1 and L), then — for
+// columns on a vertical element face (gx or gy a multiple of n1) — the nodes
+// of layer L's interior planes, whose copies differ only by k within the
+// same 2 or 4 elements (all their loads issued before any sum), and the top
+// plane for the slab's last layer.
+template <int LX, int PB>
+__global__ void __launch_bounds__(128, 8) gs_follow_kernel(const FollowArgs F) {
+  constexpr int n1 = LX - 1;
+  constexpr int L2 = LX * LX;
+  constexpr int L3 = LX * LX * LX;
+  constexpr int64_t DX = L3 - n1;
+  const BoxGS& M = F.M;
+  const int NX = (int)M.NX, nx = M.nx, ny = M.ny;
+  const int64_t ncol = M.NX * M.NY;
+  const int64_t nl = M.ez1 - M.ez0;
+  const int64_t DY = (int64_t)nx * L3 - n1 * LX;
+  const int64_t DZ = (int64_t)nx * ny * L3 - n1 * L2;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double* __restrict__ w = F.w;
+  const bool trace = blockIdx.x == 0 && threadIdx.x == 0 && nl + 2 <= 1024;
+  if (trace) g_follow_trace[0] = gtimer();
+  for (int64_t L = 0; L < nl; ++L) {
+    const int64_t gzf = (M.ez0 + L) * n1;  // face plane below layer L
+    const bool face_ok = gzf >= F.zlo && gzf <= F.zhi;
+    const bool top_ok = (L == nl - 1) && gzf + n1 <= F.zhi;
+    if (threadIdx.x == 0) {  // the face plane below layer L also has copies in layer L - 1
+      uint64_t t0 = 0;
+      while (!layer_complete(F, L - 1) || !layer_complete(F, L)) {
+        __nanosleep(256);
+        const uint64_t t = gtimer();
+        if (t0 == 0) t0 = t;
+        if (t - t0 > 10000000000ull) __trap();  // 10 s without progress: fail loudly, never hang
+      }
+      if (trace) g_follow_trace[1 + L] = gtimer();
+    }
+    __syncthreads();
+    for (int64_t col = tg; col < ncol; col += T) {
+      const int gy = (int)(col / NX), gx = (int)(col - (int64_t)gy * NX);
+      const int qx = gx / n1, rx = gx - qx * n1, qy = gy / n1, ry = gy - qy * n1;
+      const int ex0 = (rx == 0 && qx > 0) ? qx - 1 : (qx < nx ? qx : nx - 1);
+      const int ey0 = (ry == 0 && qy > 0) ? qy - 1 : (qy < ny ? qy : ny - 1);
+      const int cx = (rx == 0 && qx > 0 && qx < nx) ? 2 : 1;
+      const int cy = (ry == 0 && qy > 0 && qy < ny) ? 2 : 1;
+      // copy (layer L, ey0, ex0) at k = 0
+      const int64_t off = ((L * ny + ey0) * (int64_t)nx + ex0) * L3 + (int64_t)(gy - ey0 * n1) * LX +
+                          (gx - ex0 * n1);
+      if (face_ok) {
+        const int cz = L > 0 ? 2 : 1;
+        if (cx * cy * cz >= 2) {
+          double v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // c = (dz, dy, dx): ascending (ez, ey, ex)
+            const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+            const bool ok = dx < cx && dy < cy && (cz == 2 ? true : dz == 1);
+            v[c] = ok ? __ldcg(w + off - (1 - dz) * DZ + dy * DY + dx * DX) : 0.0;
+          }
+          double sum = 0.0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+            if (dx < cx && dy < cy && (cz == 2 || dz == 1)) sum = __dadd_rn(sum, v[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+            if (dx < cx && dy < cy && (cz == 2 || dz == 1)) __stcg(w + off - (1 - dz) * DZ + dy * DY + dx * DX, sum);
+          }
+        }
+      }
+      if (cx * cy < 2) continue;  // interior-plane nodes off the vertical faces are unshared
+      const int rend = top_ok ? n1 : n1 - 1;
+#pragma unroll
+      for (int r0 = 1; r0 <= n1; r0 += PB) {
+        if (r0 > rend) break;
+        double v[PB][4];
+#pragma unroll
+        for (int b = 0; b < PB; ++b)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int dy = c >> 1, dx = c & 1;
+            const bool ok = r0 + b <= rend && dx < cx && dy < cy;
+            v[b][c] = ok ? __ldcg(w + off + (r0 + b) * L2 + dy * DY + dx * DX) : 0.0;
+          }
+#pragma unroll
+        for (int b = 0; b < PB; ++b) {
+          if (r0 + b > rend) break;
+          double sum = 0.0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if ((c & 1) < cx && (c >> 1) < cy) sum = __dadd_rn(sum, v[b][c]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if ((c & 1) < cx && (c >> 1) < cy) __stcg(w + off + (r0 + b) * L2 + (c >> 1) * DY + (c & 1) * DX, sum);
+        }
+      }
+    }
+  }
+  if (trace) g_follow_trace[nl + 1] = gtimer();
+}
+
+cudaError_t gs_box_follow(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                          int64_t zhi, const unsigned* progress, int64_t l0, int64_t l1, cudaStream_t st) {
+  const int n1 = lx - 1;
+  BoxGS M{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1};
+  FollowArgs F{w, M, progress, l0, l1, (int64_t)nx * ny, (int)zlo, (int)zhi};
+  if (zhi < zlo) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // two 128-thread CTAs (<= 64 registers) per SM: they must fit beside the
+  // apply's persistent CTAs; they spin only in thread 0, with nanosleep,
+  // while the other threads wait at a barrier)
+  // The follower never leaves an SM until the apply has finished, so it must
+  // not pin an SM to an L1-heavy carveout the apply's CTAs cannot use: ask
+  // for the maximum shared-memory carveout, like the apply kernels.
+  switch (lx) {
+#define AXB_FOL(N) \
+  case N:          \
+    cudaFuncSetAttribute(gs_follow_kernel<N, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                         (int)cudaSharedmemCarveoutMaxShared); \
+    gs_follow_kernel<N, 4><<<2 * sms, 128, 0, st>>>(F); \
+    break;
+    AXB_FOL(2) AXB_FOL(3) AXB_FOL(4) AXB_FOL(5) AXB_FOL(6) AXB_FOL(7) AXB_FOL(8) AXB_FOL(9)
+    AXB_FOL(10) AXB_FOL(11) AXB_FOL(12) AXB_FOL(13) AXB_FOL(14) AXB_FOL(15) AXB_FOL(16)
+#undef AXB_FOL
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+}  // namespace axb
+
+namespace axb {
+// enqueue the local DSSUM of node planes [zlo, zhi] (validated by the caller)
+cudaError_t gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                         int64_t zhi, cudaStream_t st) {
+  const int n1 = lx - 1;
+  BoxGS M{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1};
+  if (zhi < zlo) return cudaSuccess;
+  switch (lx) {
+#define AXB_GSR(N) \
+  case N:          \
+    gs_box_local_range<N>(w, M, (int)zlo, (int)zhi, st); \
+    break;
+    AXB_GSR(2) AXB_GSR(3) AXB_GSR(4) AXB_GSR(5) AXB_GSR(6) AXB_GSR(7) AXB_GSR(8) AXB_GSR(9)
+    AXB_GSR(10) AXB_GSR(11) AXB_GSR(12) AXB_GSR(13) AXB_GSR(14) AXB_GSR(15) AXB_GSR(16)
+#undef AXB_GSR
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+const char* gs_box_range_check(int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
+                               int64_t zhi) {
+  if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez1 <= ez0 || ez0 < 0) return "bad sizes";
+  const int n1 = lx - 1;
+  if (zhi >= zlo && (zlo < ez0 * n1 || zhi > ez1 * n1)) return "node planes outside the slab";
+  if ((int64_t)ny * n1 + 1 > 65535 || ez1 * n1 >= (int64_t)1 << 31 || zhi - zlo + 1 > 65535)
+    return "mesh too large for the structured path";
+  return nullptr;
+}
+}  // namespace axb
+
+// Local DSSUM restricted to node planes [zlo, zhi] (global z node-plane
+// indices inside the slab).  Lets a caller sum the planes whose copies are
+// all computed while the w they touch is still in L2 (axhelm_ax_gs_box).
+// Same per-node order as op 0.
+// debug/profiling: the follower alone on a finished apply (every layer complete)
+extern "C" int axhelm_debug_follow_only(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                                        int64_t zlo, int64_t zhi, void* stream) {
+  return cuda_status(axb::gs_box_follow(w, nx, ny, lx, ez0, ez1, zlo, zhi, nullptr, 0, 0,
+                                        (cudaStream_t)stream), "axhelm_debug_follow_only");
+}
+
+extern "C" int axhelm_debug_follow_trace(unsigned long long* out, int n) {
+  if (n > 1024) n = 1024;
+  return cuda_status(cudaMemcpyFromSymbol(out, axb::g_follow_trace, sizeof(unsigned long long) * n),
+                     "axhelm_debug_follow_trace");
+}
+
+extern "C" int axhelm_gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                                   int64_t zlo, int64_t zhi, void* stream) {
+  if (const char* why = axb::gs_box_range_check(nx, ny, lx, ez0, ez1, zlo, zhi))
+    return set_status(AXHELM_EINVAL, "axhelm_gs_box_range: %s", why);
+  return cuda_status(axb::gs_box_range(w, nx, ny, lx, ez0, ez1, zlo, zhi, (cudaStream_t)stream),
+                     "axhelm_gs_box_range");
 }

@@ -9,12 +9,20 @@ SPEC.md:14).  Per apply on rank r of a z-slab partition:
              -> PARTIAL top plane -> NCCL send up / recv from below
              -> FINISH bottom plane -> NCCL send down / recv from above
              -> WRITE top plane
-  stream S1: ax on the interior element layers            (overlaps the exchange)
-  S0 waits S1 -> local DSSUM of every other shared node
+  stream S1: ax on the interior element layers + the local DSSUM of every
+             other shared node                              (overlaps the exchange)
+  S0 waits S1
 
+The local part is one axhelm_ax_gs_box call.  Its schedules: "sequential"
+(default) — the apply streams w out, then one DSSUM pass; "follow" — a
+concurrent follower kernel sums each element layer's node planes as soon as
+the apply has finished that layer, while its w is still in L2; n — layer
+blocks with kernel boundaries.  Measured at C2 the follower,
+limited to the threads that fit beside the apply's persistent CTAs, cannot
+hide its L2 latency and the sequential pass wins.
 Interface nodes are only touched by the plane steps and local nodes only by
-the local step, so the two streams never write the same point; the result
-is bit-identical to the single-domain DSSUM (dist.py).
+the local step, so the streams never write the same point; the result is
+bit-identical to the single-domain DSSUM (dist.py) for every schedule.
 """
 
 from __future__ import annotations
@@ -33,8 +41,11 @@ FIELDS = ("h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d")
 class HelmholtzOperator:
     """w = DSSUM(A_local u) on this rank's slab; geometry resident in HBM."""
 
+    SCHEDULES = {"follow": -1, "sequential": 0}
+
     def __init__(self, mesh: BoxMesh, torch, device, comm=None, mode: str = "fast",
-                 geometry: dict | None = None, amp: float = 0.1, overlap: bool = True):
+                 geometry: dict | None = None, amp: float = 0.1, overlap: bool = True,
+                 schedule: str | int = "sequential"):
         self.mesh = mesh
         self.torch = torch
         self.device = device
@@ -50,6 +61,17 @@ class HelmholtzOperator:
         self.L3 = mesh.lx ** 3
         self._part = {}
         self._dots = torch.zeros(3, dtype=torch.float64, device=device)
+        # ax + local DSSUM schedule (axhelm_ax_gs_box): "sequential" = apply
+        # then a separate DSSUM pass (default: fastest measured);
+        # "follow" = the DSSUM runs concurrently, layer by layer behind the
+        # apply, on w still in L2; n > 0 = blocks of n element layers separated
+        # by kernel boundaries
+        self.schedule = self.SCHEDULES[schedule] if isinstance(schedule, str) else int(schedule)
+        n1 = mesh.n1
+        nl = mesh.ez1 - mesh.ez0
+        self.zlo = mesh.ez0 * n1 + (1 if mesh.rank > 0 else 0)
+        self.zhi = mesh.ez1 * n1 - (1 if mesh.rank < mesh.world - 1 else 0)
+        self._progress = torch.zeros(max(nl, 1), dtype=torch.int32, device=device)
 
     # ----------------------------------------------------------- pieces
 
@@ -81,11 +103,31 @@ class HelmholtzOperator:
         if rc:
             raise DeviceError(_lib.last_error(self.lib))
 
+    def ax_gs(self, u, w, l0: int, l1: int, stream=None, dot=None):
+        """ax on local element layers [l0, l1) and the local DSSUM of every
+        owned node plane, per self.schedule (layers outside [l0, l1) must
+        already be applied on this stream's timeline)."""
+        m = self.mesh
+        ptrs = [w.data_ptr(), u.data_ptr()] + [self.mats[k].data_ptr() for k in
+                                               ("dxd", "dyd", "dzd", "dxtd", "dytd", "dztd")]
+        ptrs += [self.geom[f].data_ptr() for f in FIELDS]
+        if stream is None:
+            stream = self.torch.cuda.current_stream(self.device)
+        part = self._partials(stream) if dot is not None else None
+        rc = self.lib.axhelm_ax_gs_box(*ptrs, m.nx, m.ny, m.lx, m.ez0, m.ez1, l0, l1, self.zlo, self.zhi,
+                                       self.mode, self.schedule, self._progress.data_ptr(),
+                                       part.data_ptr() if part is not None else None,
+                                       dot.data_ptr() if dot is not None else None,
+                                       ctypes.c_void_p(stream.cuda_stream))
+        if rc:
+            raise DeviceError(_lib.last_error(self.lib))
+
     def _partials(self, stream):
         """Per-stream scratch for the fused dot's block partials."""
         key = stream.cuda_stream
         if key not in self._part:
-            nb = self.lib.axhelm_reduce_blocks(self.mesh.nel * self.L3)
+            nb = max(self.lib.axhelm_reduce_blocks(self.mesh.nel * self.L3),
+                     self.lib.axhelm_ax_gs_scratch(self.mesh.ez1 - self.mesh.ez0))
             self._part[key] = self.torch.empty(max(nb, 2048), dtype=self.torch.float64, device=self.device)
         return self._part[key]
 
@@ -95,9 +137,10 @@ class HelmholtzOperator:
         before assembly (= <u, QQ^T A u> for continuous u; PCG's p.Ap)."""
         m = self.mesh
         torch = self.torch
+        nl = m.ez1 - m.ez0
         if not self.overlap:
-            self.ax(u, w, dot=dot)
-            self.dssum(w)
+            self.ax_gs(u, w, 0, nl, dot=dot)
+            self._exchange(w)
             return w
         s0 = torch.cuda.current_stream(self.device)
         lay = m.nx * m.ny
@@ -107,7 +150,18 @@ class HelmholtzOperator:
         self.ax(u, w, m.nel - lay, m.nel, dot=d3[1:2] if d3 is not None else None)
         self.side.wait_stream(s0)
         with torch.cuda.stream(self.side):
-            self.ax(u, w, lay, m.nel - lay, stream=self.side, dot=d3[2:3] if d3 is not None else None)
+            # interior layers + every local DSSUM plane
+            self.ax_gs(u, w, 1, nl - 1, stream=self.side, dot=d3[2:3] if d3 is not None else None)
+        self._exchange(w)
+        s0.wait_stream(self.side)
+        if dot is not None:
+            dot.copy_(d3.sum().reshape(dot.shape))
+        return w
+
+    def _exchange(self, w):
+        """Interface planes: PARTIAL (top) -> send up -> FINISH (bottom) ->
+        send down -> WRITE (top).  Touches only interface-plane points."""
+        m = self.mesh
         d = self.dssum
         if d.has_top:
             self.gs.plane(0, "top", w, d.buf_top)
@@ -119,11 +173,6 @@ class HelmholtzOperator:
             d.comm.sendrecv(send=d.buf_bot if d.has_bot else None, dst=m.rank - 1,
                             recv=d.buf_top if d.has_top else None, src=m.rank + 1)
         d.phase_write(w)
-        s0.wait_stream(self.side)
-        self.gs.sum_local(w)
-        if dot is not None:
-            dot.copy_(d3.sum().reshape(dot.shape))
-        return w
 
     def bytes_per_apply(self) -> int:
         return 72 * self.mesh.nel * self.L3 + self.gs.bytes_per_apply()
