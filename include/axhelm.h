@@ -158,7 +158,7 @@ int axhelm_gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t 
  *       completion counters in progress[l1 - l0] (zeroed here); a DSSUM
  *       follower kernel runs concurrently on an internal stream (joined back
  *       into `stream`) and sums each layer's planes as soon as it is
- *       complete (TMA-ring kernels, lx <= 12; else sequential);
+ *       complete (the lx = 8 FAST DMMA kernel; else sequential);
  *   n > 0: blocks of n layers, each apply followed by the DSSUM of the planes
  *       it completes (kernel-boundary version of FOLLOW).
  * dot_out (nullable): sum_p u_p (A u)_p over the applied elements before

@@ -60,7 +60,7 @@ __device__ __forceinline__ int ut_idx(int l, int j, int i) {
 // order) into dot_partial[blockIdx.x] — the PCG's <p, A p> without a pass.
 template <bool DOT>
 __global__ void __launch_bounds__(DmCfg::NT)
-ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
+ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, const AxExt X) {
   using C = DmCfg;
   constexpr int FIELD = C::FIELD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -73,7 +73,7 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
   const int lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int64_t stride = gridDim.x;
-  const L2Pol pol = make_l2pol(A.keep_w);
+  const L2Pol pol = make_l2pol(X.keep_w);
 
   if (tid == 0) {
     for (int d = 0; d < C::D; ++d) mbar_init(&bars[d], 1);
@@ -220,7 +220,7 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial) {
     }
     __syncthreads();  // buffer b and ST free
     if (tid == 0) {
-      if (A.progress) signal_done(A, e, 1);
+      if (X.progress) signal_done(X, e, 1);
       const int64_t en = e + C::D * stride;
       if (en < nel) {
         fence_proxy_async();

@@ -50,6 +50,12 @@ struct AxPtrs {
   const double* __restrict__ g12;
   const double* __restrict__ g13;
   const double* __restrict__ g23;
+};
+
+// Per-call extensions honoured by the lx = 8 DMMA kernel only (kept out of
+// AxPtrs: growing the vector kernels' parameter block shifted ptxas's
+// register allocation and cost up to 35% at lx = 10).
+struct AxExt {
   // 1: the caller reads w again soon (layer-blocked ax + DSSUM): inputs are
   // loaded L2 evict-first and w is stored evict-normal so it stays in L2;
   // 0 (default): w is streamed out evict-first.
@@ -64,12 +70,12 @@ struct AxPtrs {
 // Thread 0, after a __syncthreads that follows every thread's w stores of
 // elements [e0, e0 + ne): publish them (the CUTLASS semaphore pattern: the
 // barrier orders the CTA's stores before thread 0's release).
-__device__ __forceinline__ void signal_done(const AxPtrs& A, int64_t e0, int64_t ne) {
+__device__ __forceinline__ void signal_done(const AxExt& X, int64_t e0, int64_t ne) {
   const int64_t end = e0 + ne;
   for (int64_t e = e0; e < end;) {
-    const int64_t L = e / A.lay;
-    const int64_t stop = (L + 1) * A.lay < end ? (L + 1) * A.lay : end;
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(A.progress + L), "r"((unsigned)(stop - e))
+    const int64_t L = e / X.lay;
+    const int64_t stop = (L + 1) * X.lay < end ? (L + 1) * X.lay : end;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(X.progress + L), "r"((unsigned)(stop - e))
                  : "memory");
     e = stop;
   }
@@ -137,19 +143,14 @@ __device__ __forceinline__ L2Pol make_l2pol(int keep_w) {
   }
   return P;
 }
-// w store: streamed (evict-first) unless the policy keeps w in L2
+// w store with the policy's L2 hint (evict-first = streamed, or evict-normal
+// when w is read again soon); no branch, the policy is a register operand
 __device__ __forceinline__ void stg_w(double* p, double v, const L2Pol& P) {
-  if (P.keep)
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(P.w) : "memory");
-  else
-    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(P.w) : "memory");
 }
 __device__ __forceinline__ void stg_w2(double* p, double v0, double v1, const L2Pol& P) {
-  if (P.keep)
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v0), "d"(v1), "l"(P.w)
-                 : "memory");
-  else
-    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v0), "d"(v1) : "memory");
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v0), "d"(v1), "l"(P.w)
+               : "memory");
 }
 
 // v1 k-walk kernel: one CTA per EPB elements.

@@ -16,15 +16,17 @@ int default_mode();
 // enqueue one apply over device pointers (no validation).  hz / hzt / hx /
 // hxt: host copies of dzd / dztd / dxd / dxtd when the caller has them
 // (else looked up in / added to the pointer-keyed cache).
+// X: keep-w-in-L2 / progress extensions (honoured by the lx = 8 DMMA kernel)
 cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
                       const double* hz = nullptr, const double* hzt = nullptr,
-                      const double* hx = nullptr, const double* hxt = nullptr);
+                      const double* hx = nullptr, const double* hxt = nullptr,
+                      const AxExt& X = AxExt{});
 
 // fused lx = 8 fast apply + per-CTA partials of sum u*w (nparts written)
 cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int* nparts,
-                             cudaStream_t st);
-// true when launch_ax would run a kernel that honours AxPtrs::progress
-// (the TMA-ring kernels: lx <= 12, 16-B aligned fields)
+                             cudaStream_t st, const AxExt& X = AxExt{});
+// true when launch_ax would run a kernel that honours AxExt (the lx = 8
+// DMMA kernel; callers also check mode FAST via dmma8_selected)
 bool progress_capable(const AxPtrs& A, int lx);
 // true when launch_ax would run the fused-capable DMMA kernel
 bool dmma8_selected(const AxPtrs& A, int lx, int mode);

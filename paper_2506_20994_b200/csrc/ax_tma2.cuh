@@ -70,7 +70,7 @@ struct T2Cfg {
 // arrive + cooperative load.  Returns pad, or -1 for the fallback.
 template <int LX, int NKS>
 __device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
-                                            uint64_t* bar, uint64_t pol) {
+                                            uint64_t* bar) {
   using C = T2Cfg<LX, NKS>;
   const int64_t e0 = g * C::EPL;
   const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
@@ -84,7 +84,7 @@ __device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_
   const uint32_t bytes = (uint32_t)((hi - lo) * 8);
   mbar_arrive_expect_tx(bar, 8u * bytes);
 #pragma unroll
-  for (int f = 0; f < 8; ++f) bulk_g2s_hint(buf + f * C::FSTRIDE, field_ptr(A, f) + lo, bytes, bar, pol);
+  for (int f = 0; f < 8; ++f) bulk_g2s(buf + f * C::FSTRIDE, field_ptr(A, f) + lo, bytes, bar);
   return pad;
 }
 
@@ -147,8 +147,7 @@ __device__ __forceinline__ void stage1(const TParams<LX>& P, const double* sZ, c
 template <int LX, bool FAST, int NKS, int KH, bool UP>
 __device__ __forceinline__ void stage2(const TParams<LX>& P, const double* sZt, const ElemView& v,
                                        const double (&dxtr)[LX], const double (&dytr)[LX], int j,
-                                       int i, const double (&utr_in)[LX], double* wout, bool active,
-                                       const L2Pol& pol) {
+                                       int i, const double (&utr_in)[LX], double* wout, bool active) {
   using C = T2Cfg<LX, NKS>;
   constexpr int L2 = C::L2;
   const int p = j * LX + i;
@@ -176,7 +175,7 @@ __device__ __forceinline__ void stage2(const TParams<LX>& P, const double* sZt, 
       w = madd<FAST>(w, dytr[l], sc[l]);
       w = madd<FAST>(w, ztval<LX, UP>(P, sZt, k, l), utc[l]);
     }
-    if (active) stg_w(wout + k * L2, w, pol);
+    if (active) stg_stream(wout + k * L2, w);
   }
 }
 
@@ -205,19 +204,18 @@ template <int LX, bool FAST, int NKS, bool UP>
 __device__ __forceinline__ void stage2_dispatch(int kh, const TParams<LX>& P, const double* sZt,
                                                 const ElemView& v, const double (&dxtr)[LX],
                                                 const double (&dytr)[LX], int j, int i,
-                                                const double (&utr)[LX], double* wout, bool active,
-                                                const L2Pol& pol) {
+                                                const double (&utr)[LX], double* wout, bool active) {
   if constexpr (NKS == 1) {
-    stage2<LX, FAST, 1, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol);
+    stage2<LX, FAST, 1, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
   } else if constexpr (NKS == 2) {
-    if (kh == 0) stage2<LX, FAST, 2, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol);
-    else stage2<LX, FAST, 2, 1, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol);
+    if (kh == 0) stage2<LX, FAST, 2, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
+    else stage2<LX, FAST, 2, 1, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
   } else {
     switch (kh) {
-      case 0: stage2<LX, FAST, 4, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol); break;
-      case 1: stage2<LX, FAST, 4, 1, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol); break;
-      case 2: stage2<LX, FAST, 4, 2, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol); break;
-      default: stage2<LX, FAST, 4, 3, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol); break;
+      case 0: stage2<LX, FAST, 4, 0, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active); break;
+      case 1: stage2<LX, FAST, 4, 1, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active); break;
+      case 2: stage2<LX, FAST, 4, 2, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active); break;
+      default: stage2<LX, FAST, 4, 3, UP>(P, sZt, v, dxtr, dytr, j, i, utr, wout, active); break;
     }
   }
 }
@@ -246,7 +244,6 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
   const int i = p - j * LX;
   const int64_t ngroups = (nel + C::EPL - 1) / C::EPL;
   const int64_t stride = gridDim.x;
-  const L2Pol pol = make_l2pol(A.keep_w);
 
   if (tid == 0) {
 #pragma unroll
@@ -258,7 +255,7 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
 #pragma unroll
     for (int d = 0; d < C::D; ++d) {
       const int64_t g = blockIdx.x + d * stride;
-      if (g < ngroups) issue_group2<LX, NKS>(A, nel, g, bufs + d * C::BUF, &bars[d], pol.in);
+      if (g < ngroups) issue_group2<LX, NKS>(A, nel, g, bufs + d * C::BUF, &bars[d]);
     }
   }
   // device copy of the t-direction matrices (transposed) + verification of
@@ -313,15 +310,14 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
     else stage1_dispatch<LX, FAST, NKS, false>(kh, P, sZ, v, dxr, dyr, j, i, utr);
     __syncthreads();  // ur / us / ut of the whole element visible
     double* wout = A.w + (e0 + el) * L3 + p;
-    if (use_param) stage2_dispatch<LX, FAST, NKS, true>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol);
-    else stage2_dispatch<LX, FAST, NKS, false>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active, pol);
-    __syncthreads();  // every read of buffer b is done (and every w store issued)
+    if (use_param) stage2_dispatch<LX, FAST, NKS, true>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
+    else stage2_dispatch<LX, FAST, NKS, false>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
+    __syncthreads();  // every read of buffer b is done
     if (tid == 0) {
-      if (A.progress) signal_done(A, e0, ne);
       const int64_t gn = g + C::D * stride;
       if (gn < ngroups) {
         fence_proxy_async();
-        issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b], pol.in);
+        issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
       }
     }
   }

@@ -222,16 +222,16 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
   return (int)(grid > nel ? nel : grid);
 }
 
-static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st) {
+static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st, const AxExt& X) {
   cudaError_t e;
   const int grid = dmma8_grid(nel, &e);
   if (e != cudaSuccess) return e;
-  ax_dmma8<false><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, nullptr);
+  ax_dmma8<false><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, nullptr, X);
   return cudaGetLastError();
 }
 
 bool progress_capable(const AxPtrs& A, int lx) {
-  return lx <= 12 && (g_variant == 0 || g_variant == 4 || g_variant == 6) && aligned16(A);
+  return lx == 8 && (g_variant == 0 || g_variant == 6) && aligned16(A);
 }
 
 bool dmma8_selected(const AxPtrs& A, int lx, int mode) {
@@ -240,11 +240,11 @@ bool dmma8_selected(const AxPtrs& A, int lx, int mode) {
 
 // fused apply + sum u*w (lx = 8, fast): per-CTA partials, fixed-order reduce
 cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int* nparts,
-                             cudaStream_t st) {
+                             cudaStream_t st, const AxExt& X) {
   cudaError_t e;
   const int grid = dmma8_grid(nel, &e);
   if (e != cudaSuccess) return e;
-  ax_dmma8<true><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial);
+  ax_dmma8<true><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial, X);
   *nparts = grid;
   return cudaGetLastError();
 }
@@ -280,11 +280,12 @@ static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 
 template <int LX, bool FAST>
 static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
-                                  const double* hzt, const double* hx, const double* hxt) {
+                                  const double* hzt, const double* hx, const double* hxt,
+                                  const AxExt& X) {
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
   if constexpr (LX <= 8) {
     if ((g_variant == 6 || g_variant == 0) && FAST && aligned16(A)) {
-      if constexpr (LX == 8) return launch_dmma8(A, nel, st);
+      if constexpr (LX == 8) return launch_dmma8(A, nel, st, X);
     }
   }
   if constexpr (LX <= 12) {
@@ -306,18 +307,19 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
 template <int LX>
 static cudaError_t launch_lx(const AxPtrs& A, int64_t nel, int mode, cudaStream_t st,
                              const double* hz, const double* hzt, const double* hx,
-                             const double* hxt) {
-  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, hx, hxt)
-                             : launch_variant<LX, false>(A, nel, st, hz, hzt, hx, hxt);
+                             const double* hxt, const AxExt& X) {
+  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, hx, hxt, X)
+                             : launch_variant<LX, false>(A, nel, st, hz, hzt, hx, hxt, X);
 }
 
 cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
-                      const double* hz, const double* hzt, const double* hx, const double* hxt) {
+                      const double* hz, const double* hzt, const double* hx, const double* hxt,
+                      const AxExt& X) {
   if (nel == 0) return cudaSuccess;
   switch (lx) {
 #define AXB_CASE(N) \
   case N:           \
-    return launch_lx<N>(A, nel, mode, st, hz, hzt, hx, hxt);
+    return launch_lx<N>(A, nel, mode, st, hz, hzt, hx, hxt, X);
     AXB_CASE(2) AXB_CASE(3) AXB_CASE(4) AXB_CASE(5) AXB_CASE(6) AXB_CASE(7)
     AXB_CASE(8) AXB_CASE(9) AXB_CASE(10) AXB_CASE(11) AXB_CASE(12)
     AXB_CASE(13) AXB_CASE(14) AXB_CASE(15) AXB_CASE(16)
@@ -359,8 +361,11 @@ int axhelm_apply(double* wd, const double* ud, const double* dxd, const double* 
                             h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   for (int q = 0; q < 15; ++q)
     if (!ptrs[q]) return set_status(AXHELM_EINVAL, "argument %d is NULL", q);
-  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d, keep};
-  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream), "axhelm_apply");
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  AxExt X;
+  X.keep_w = keep;
+  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr, X),
+                     "axhelm_apply");
 }
 
 void __dace_ax_helm(double* AXH_RESTRICT wd, const double* AXH_RESTRICT ud,

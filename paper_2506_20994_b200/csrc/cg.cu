@@ -199,19 +199,19 @@ namespace axb {
 // ax_helm + out[0] = sum u*w over the nel elements (fused for the lx = 8
 // DMMA kernel, else a separate fixed-order dot pass); partial: block scratch
 static cudaError_t ax_dot(const AxPtrs& A, int64_t nel, int lx, int mode, double* partial, double* out,
-                          cudaStream_t st) {
+                          cudaStream_t st, const AxExt& X = AxExt{}) {
   const int64_t n = nel * lx * lx * lx;
   cudaError_t e;
   if (dmma8_selected(A, lx, mode)) {
     int nb = 0;
-    e = launch_dmma8_dot(A, nel, partial, &nb, st);
+    e = launch_dmma8_dot(A, nel, partial, &nb, st, X);
     if (e == cudaSuccess) {
       reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 1, out);
       e = cudaGetLastError();
     }
     return e;
   }
-  e = launch_ax(A, nel, lx, mode, st);
+  e = launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
   if (e == cudaSuccess) {
     const int nb = red_blocks(n);
     dot_kernel<<<nb, RT, 0, st>>>(A.u, A.w, nullptr, n, partial);
@@ -264,12 +264,14 @@ int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const doub
   mode &= ~AXHELM_KEEP_W_L2;
   if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
     return set_status(AXHELM_EINVAL, "axhelm_apply_dot: unknown mode %d", mode);
-  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d, keep};
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  AxExt X;
+  X.keep_w = keep;
   if (nel == 0) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream);
     return cuda_status(e, "axhelm_apply_dot");
   }
-  return cuda_status(ax_dot(A, nel, lx, mode, partial, out, (cudaStream_t)stream), "axhelm_apply_dot");
+  return cuda_status(ax_dot(A, nel, lx, mode, partial, out, (cudaStream_t)stream, X), "axhelm_apply_dot");
 }
 
 int axhelm_ax_gs_scratch(int64_t nlayers) { return max_partials() + (int)(nlayers > 0 ? nlayers : 0); }
@@ -295,19 +297,21 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
   const int64_t L3 = (int64_t)lx * lx * lx, lay = (int64_t)nx * ny;
   const int pmax = max_partials();
   double* chunk_dot = partial ? partial + pmax : nullptr;
-  auto ptrs_at = [&](int64_t layer, int keep) {
+  auto ptrs_at = [&](int64_t layer) {
     const int64_t o = layer * lay * L3;
     return AxPtrs{wd + o, ud + o, dxd, dyd, dzd, dxtd, dytd, dztd, h1d + o, g11d + o, g22d + o, g33d + o,
-                  g12d + o, g13d + o, g23d + o, keep};
+                  g12d + o, g13d + o, g23d + o};
   };
   cudaError_t e = cudaSuccess;
   if (schedule == AXHELM_SCHED_FOLLOW) {
-    AxPtrs A = ptrs_at(l0, 1);
-    A.progress = progress;
-    A.lay = lay;
-    // the dot of the non-fused kernels is a separate pass over w, which the
-    // follower is already assembling: those run the sequential schedule
-    if (l1 > l0 && progress_capable(A, lx) && (!dot_out || dmma8_selected(A, lx, mode))) {
+    AxPtrs A = ptrs_at(l0);
+    AxExt X;
+    X.keep_w = 1;
+    X.progress = progress;
+    X.lay = lay;
+    // only the lx = 8 DMMA kernel publishes progress (its dot is fused, taken
+    // before the follower assembles w); everything else runs sequentially
+    if (l1 > l0 && progress_capable(A, lx) && dmma8_selected(A, lx, mode)) {
       FollowStreams* fs = follow_streams();
       if (!fs) return set_status(AXHELM_ECUDA, "axhelm_ax_gs_box: cannot create the follower stream");
       // The apply is enqueued first and never waits on the follower, so it
@@ -318,8 +322,8 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
       if (e == cudaSuccess) e = cudaEventRecord(fs->fork, st);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(fs->side, fs->fork, 0);
       if (e == cudaSuccess)
-        e = dot_out ? ax_dot(A, (l1 - l0) * lay, lx, mode, partial, dot_out, st)
-                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st);
+        e = dot_out ? ax_dot(A, (l1 - l0) * lay, lx, mode, partial, dot_out, st, X)
+                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
       if (e == cudaSuccess) e = gs_box_follow(wd, nx, ny, lx, ez0, ez1, zlo, zhi, progress, l0, l1, fs->side);
       if (e == cudaSuccess) e = cudaEventRecord(fs->join, fs->side);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(st, fs->join, 0);
@@ -332,9 +336,12 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
   int nchunks = 0;
   for (int64_t a = l0; a < l1 && e == cudaSuccess; a += B, ++nchunks) {
     const int64_t b = (a + B < l1) ? a + B : l1;
-    AxPtrs A = ptrs_at(a, schedule > 0 ? 1 : 0);
+    AxPtrs A = ptrs_at(a);
+    AxExt X;
+    X.keep_w = schedule > 0 ? 1 : 0;
     const int64_t nel = (b - a) * lay;
-    e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st) : launch_ax(A, nel, lx, mode, st);
+    e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st, X)
+                : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
     if (e != cudaSuccess) break;
     // planes whose every copy is computed: below layer ez0 + b, or all when
     // the layers above l1 are done by the caller

@@ -225,3 +225,15 @@ def test_matrix_changed_in_place_is_honoured(torch, kern):
             kern["strict"](dev, nel, lx)
             torch.cuda.synchronize()
             assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays)), name
+
+
+@pytest.mark.parametrize("lx", [9, 10, 11, 12])
+def test_fast_large_lx_ring_reuse(torch, kern, lx):
+    """lx 9..12 fast mode (one element per CTA-iteration of the TMA ring): more
+    elements than resident CTAs (ring reuse, both parities of the element
+    offset for odd lx^3, the tail element) against the oracle at 1e-12."""
+    for nel in (1, 149, 297 + (lx % 2)):
+        arrays = o.problem(lx, nel, seed=11)
+        got = run_dev(torch, kern["fast"], arrays, nel, lx)
+        assert np.isfinite(got).all(), (lx, nel)
+        assert o.normwise_rel(got, o.ax(arrays)) <= FAST_TOL, (lx, nel)
