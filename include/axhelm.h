@@ -200,6 +200,19 @@ int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const doub
                      const double* h1d, const double* g11d, const double* g22d, const double* g33d,
                      const double* g12d, const double* g13d, const double* g23d, int64_t nel,
                      int lx, int mode, double* partial, double* out, void* stream);
+/* Structured-brick PCG update with the local DSSUM folded in: w = A_local p
+ * after the interface-plane exchange (axhelm_gs_box ops 1..3) but WITHOUT the
+ * local DSSUM; each point gathers its node's local copies in the DSSUM's
+ * order (bit-identical assembled value), r -= (a[0]/a[1]) QQ^T w, and
+ * out = (sum cwt r dinv r, sum cwt r r) with cwt = mask/multiplicity computed
+ * from the point's position (mask: the brick's outer boundary).  The slab is
+ * element layers [ez0, ez1) of an nx*ny*nz brick. */
+int axhelm_cg_update_box(double* r, const double* w, const double* dinv, const double* a, int nx,
+                         int ny, int64_t nz, int lx, int64_t ez0, int64_t ez1, int has_below,
+                         int has_above, double* partial, double* out, void* stream);
+/* x += (a[0]/a[1]) p; p = dinv r + (sc_new[0]/a[0]) p  (a = (rz_old, p.Ap)) */
+int axhelm_cg_xpupdate(double* x, double* p, const double* r, const double* dinv, const double* a,
+                       const double* sc_new, int64_t n, void* stream);
 /* p = dinv r + (sc_new[0]/sc_old[0]) p */
 int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const double* sc_new,
                       const double* sc_old, int64_t n, void* stream);

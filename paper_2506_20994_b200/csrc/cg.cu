@@ -11,10 +11,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/axhelm.h"
 #include "ax_launch.h"
+#include "box_gs.cuh"
 
 namespace axb {
 
@@ -104,6 +106,122 @@ __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
   write_partials<2>(v, partial);
 }
 
+// Structured-brick variant of cg_update with the local DSSUM folded in
+// (no separate pass over w): w holds A_local p (after the interface-plane
+// exchange, whose points already carry their final sums); every other point
+// gathers its node's local copies in ascending local order — the DSSUM's own
+// order, so the assembled value is bit-identical — and cwt = mask / mult is
+// computed from the point's position (exact powers of two).
+//   alpha = a[0] / a[1];  r -= alpha (QQ^T w);  partial: rz', rr as cg_update
+// x is not touched here (cg_xpupdate advances it with the old p).
+struct CgBox {
+  BoxGS M;
+  int64_t NZ;  // global node planes
+  int has_below, has_above;
+};
+
+// One element per block iteration (grid-stride over elements): the
+// element's brick coordinates are computed once; a point's copies follow
+// from which of its faces are interior (the lowest copy is q minus the
+// strides of its lower neighbours, the others the compile-time / per-mesh
+// strides above it — the order of gs_box_copies); branch-free so the loads
+// of a thread's points overlap.
+// EPI elements per iteration, MINB resident blocks per SM (register cap):
+// (1, 3) measured best at lx = 8 (0.94 ms at C2 vs 1.0-2.1 ms for (1, 1..8),
+// (2, 1..4), (4, 2): profiles/r01_cg_update_box.txt)
+template <int LX, int EPI, int MINB>
+__global__ void __launch_bounds__(RT, MINB) cg_update_box_kernel(double* __restrict__ r, const double* __restrict__ w,
+                                                           const double* __restrict__ dinv,
+                                                           const double* __restrict__ a, const CgBox B,
+                                                           int64_t nel, double* __restrict__ partial) {
+  constexpr int n1 = LX - 1, L2 = LX * LX, L3 = L2 * LX;
+  constexpr int PPT = (L3 + RT - 1) / RT;  // points per thread per element
+  constexpr int NP = EPI * PPT;            // EPI elements per iteration: all loads issued first
+  constexpr int64_t DX = L3 - n1;
+  const BoxGS& M = B.M;
+  const int64_t DY = (int64_t)M.nx * L3 - n1 * LX;
+  const int64_t DZ = (int64_t)M.nx * M.ny * L3 - n1 * L2;
+  const int nl = (int)(M.ez1 - M.ez0);
+  const double alpha = a[0] / a[1];
+  double v[2] = {0.0, 0.0};
+  for (int64_t e0 = (int64_t)blockIdx.x * EPI; e0 < nel; e0 += (int64_t)gridDim.x * EPI) {
+    double c8[NP][8], rq[NP], dq[NP], cw[NP];
+    int64_t qq[NP];
+    bool act[NP], single[NP];
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      const int64_t e = e0 + u / PPT;
+      const int p = threadIdx.x + (u % PPT) * RT;
+      act[u] = e < nel && (PPT * RT == L3 || p < L3);
+      const int ei = act[u] ? (int)e : 0;
+      const int pi = act[u] ? p : 0;
+      const int t = ei / M.nx;
+      const int ex = ei - t * M.nx;
+      const int ezl = t / M.ny;
+      const int ey = t - ezl * M.ny;
+      const int k = pi / L2, j = (pi / LX) % LX, i = pi % LX;
+      const int64_t q = (int64_t)ei * L3 + pi;
+      qq[u] = q;
+      const bool lox = i == 0 && ex > 0, hix = i == n1 && ex < M.nx - 1;
+      const bool loy = j == 0 && ey > 0, hiy = j == n1 && ey < M.ny - 1;
+      const bool iface = (k == 0 && ezl == 0 && B.has_below) || (k == n1 && ezl == nl - 1 && B.has_above);
+      const bool loz = !iface && k == 0 && ezl > 0, hiz = !iface && k == n1 && ezl < nl - 1;
+      const int cx = (lox || hix) && !iface ? 2 : 1, cy = (loy || hiy) && !iface ? 2 : 1;
+      const int cz = loz || hiz ? 2 : 1;
+      single[u] = cx * cy * cz == 1;
+      const int64_t b0 = q - ((lox && !iface) ? DX : 0) - ((loy && !iface) ? DY : 0) - (loz ? DZ : 0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+        c8[u][c] = (act[u] && dz < cz && dy < cy && dx < cx) ? w[b0 + dx * DX + dy * DY + dz * DZ] : 0.0;
+      }
+      rq[u] = act[u] ? r[q] : 0.0;
+      dq[u] = act[u] ? dinv[q] : 0.0;
+      const int gx = ex * n1 + i, gy = ey * n1 + j, gz = (int)(M.ez0 + ezl) * n1 + k;
+      const bool bnd = gx == 0 || gx == M.NX - 1 || gy == 0 || gy == M.NY - 1 || gz == 0 || gz == B.NZ - 1;
+      const int mult = (i % n1 == 0 ? 2 : 1) * (j % n1 == 0 ? 2 : 1) * (k % n1 == 0 ? 2 : 1);
+      cw[u] = bnd ? 0.0 : 1.0 / (double)mult;
+    }
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      // absent copies hold +0.0: adding them is exact (a running sum that
+      // starts at +0.0 is never -0.0 under round-to-nearest), so the sum
+      // equals the DSSUM's predicated one bit for bit
+      double wa;
+      if (single[u]) {
+        wa = c8[u][0];  // unshared or interface point: w as is
+      } else {
+        wa = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) wa = __dadd_rn(wa, c8[u][c]);
+      }
+      if (!act[u]) continue;
+      const double rr = fma(-alpha, wa, rq[u]);
+      r[qq[u]] = rr;
+      const double c = cw[u] * rr;
+      v[0] += c * dq[u] * rr;
+      v[1] += c * rr;
+    }
+  }
+  write_partials<2>(v, partial);
+}
+
+// alpha = a[0] / a[1], beta = sc_new[0] / a[0] (a = (rz_old, p.Ap)):
+// x += alpha p (the old p);  p = dinv r + beta p
+__global__ void cg_xpupdate_kernel(double* __restrict__ x, double* __restrict__ p,
+                                   const double* __restrict__ r, const double* __restrict__ dinv,
+                                   const double* __restrict__ a, const double* __restrict__ sc_new,
+                                   int64_t n) {
+  const double alpha = a[0] / a[1];
+  const double beta = sc_new[0] / a[0];
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double pq = p[q];
+    x[q] = fma(alpha, pq, x[q]);
+    p[q] = fma(beta, pq, dinv[q] * r[q]);
+  }
+}
+
 // beta = sc_new[0] / sc_old[0]; p = dinv r + beta p
 __global__ void cg_pupdate_kernel(double* __restrict__ p, const double* __restrict__ r,
                                   const double* __restrict__ dinv, const double* __restrict__ sc_new,
@@ -184,6 +302,38 @@ int axhelm_cg_update(double* x, double* r, const double* p, const double* w, con
   cg_update_kernel<<<nb, RT, 0, st>>>(x, r, p, w, dinv, cwt, sc, n, partial);
   reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
   return cuda_status(cudaGetLastError(), "axhelm_cg_update");
+}
+
+int axhelm_cg_update_box(double* r, const double* w, const double* dinv, const double* a, int nx,
+                         int ny, int64_t nz, int lx, int64_t ez0, int64_t ez1, int has_below,
+                         int has_above, double* partial, double* out, void* stream) {
+  if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez0 < 0 || ez1 <= ez0 || ez1 > nz)
+    return set_status(AXHELM_EINVAL, "axhelm_cg_update_box: bad sizes");
+  const int n1 = lx - 1;
+  CgBox B{BoxGS{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1}, nz * n1 + 1,
+          has_below, has_above};
+  const int64_t nel = (ez1 - ez0) * nx * ny;
+  if (nel >= ((int64_t)1 << 31)) return set_status(AXHELM_EINVAL, "axhelm_cg_update_box: too many elements");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = red_blocks(nel * lx * lx * lx);
+  switch (lx) {
+#define AXB_CGB(N) \
+  case N:          \
+    cg_update_box_kernel<N, 1, 3><<<nb, RT, 0, st>>>(r, w, dinv, a, B, nel, partial); \
+    break;
+    AXB_CGB(2) AXB_CGB(3) AXB_CGB(4) AXB_CGB(5) AXB_CGB(6) AXB_CGB(7) AXB_CGB(8) AXB_CGB(9)
+    AXB_CGB(10) AXB_CGB(11) AXB_CGB(12) AXB_CGB(13) AXB_CGB(14) AXB_CGB(15) AXB_CGB(16)
+#undef AXB_CGB
+  }
+  reduce_partials_kernel<<<1, RT, 0, st>>>(partial, nb, 2, out);
+  return cuda_status(cudaGetLastError(), "axhelm_cg_update_box");
+}
+
+int axhelm_cg_xpupdate(double* x, double* p, const double* r, const double* dinv, const double* a,
+                       const double* sc_new, int64_t n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cg_xpupdate_kernel<<<red_blocks(n), RT, 0, st>>>(x, p, r, dinv, a, sc_new, n);
+  return cuda_status(cudaGetLastError(), "axhelm_cg_xpupdate");
 }
 
 int axhelm_cg_pupdate(double* p, const double* r, const double* dinv, const double* sc_new,

@@ -131,15 +131,21 @@ class HelmholtzOperator:
             self._part[key] = self.torch.empty(max(nb, 2048), dtype=self.torch.float64, device=self.device)
         return self._part[key]
 
-    def apply(self, u, w, dot=None):
+    def apply(self, u, w, dot=None, local_dssum: bool = True):
         """w = Q Q^T A u on this rank (with the interface exchange).  dot: an
         optional device scalar receiving the rank-local sum_p u_p (A u)_p
-        before assembly (= <u, QQ^T A u> for continuous u; PCG's p.Ap)."""
+        before assembly (= <u, QQ^T A u> for continuous u; PCG's p.Ap).
+        local_dssum=False leaves the local shared nodes unassembled (only the
+        interface planes are summed) for a consumer that gathers them itself
+        (axhelm_cg_update_box)."""
         m = self.mesh
         torch = self.torch
         nl = m.ez1 - m.ez0
         if not self.overlap:
-            self.ax_gs(u, w, 0, nl, dot=dot)
+            if local_dssum:
+                self.ax_gs(u, w, 0, nl, dot=dot)
+            else:
+                self.ax(u, w, dot=dot)
             self._exchange(w)
             return w
         s0 = torch.cuda.current_stream(self.device)
@@ -151,7 +157,11 @@ class HelmholtzOperator:
         self.side.wait_stream(s0)
         with torch.cuda.stream(self.side):
             # interior layers + every local DSSUM plane
-            self.ax_gs(u, w, 1, nl - 1, stream=self.side, dot=d3[2:3] if d3 is not None else None)
+            dd = d3[2:3] if d3 is not None else None
+            if local_dssum:
+                self.ax_gs(u, w, 1, nl - 1, stream=self.side, dot=dd)
+            else:
+                self.ax(u, w, lay, m.nel - lay, stream=self.side, dot=dd)
         self._exchange(w)
         s0.wait_stream(self.side)
         if dot is not None:

@@ -69,3 +69,26 @@ def test_pcg_converges_to_manufactured_solution(torch):
     h = hist.cpu().numpy()
     assert h[-1] <= 1e-20 * h[0]
     assert float((x - xs).abs().max() / xs.abs().max()) <= 1e-8
+
+
+@pytest.mark.parametrize("dims,mode", [((3, 2, 4, 5), "strict"), ((2, 3, 3, 8), "fast"), ((2, 2, 2, 3), "strict")])
+def test_fused_update_matches_separate_passes(torch, dims, mode):
+    """axhelm_cg_update_box (local DSSUM gathered inside the residual update,
+    cwt from the position) + axhelm_cg_xpupdate against the separate DSSUM
+    pass + cg_update + cg_pupdate: the per-point arithmetic is identical
+    (the gathered sum is the DSSUM's, bit for bit); only the fixed order of
+    the block reductions differs (element-major vs point-major), so the
+    iterates agree to reassociation."""
+    from paper_2506_20994_b200.cg import JacobiPCG
+
+    nx, ny, nz, lx = dims
+    m, op, pcg = _setup(torch, nx, ny, nz, lx, mode)
+    gid = m.gid(torch, "cuda")
+    f = torch.randn(int(gid.max()) + 1, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(3))[gid]
+    x1, h1 = pcg.solve(f, iters=12)
+    x1, h1 = x1.clone(), h1.clone()
+    x2, h2 = JacobiPCG(op, fused=False).solve(f, iters=12)
+    torch.cuda.synchronize()
+    assert float(((h1 - h2).abs() / h2).max()) <= 1e-10
+    assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-10
