@@ -35,24 +35,29 @@ struct TParams {
   double ztT[LX * LX];  // ztT[k][l] = dztd[l][k]
 };
 
-// Per-lx shape: elements per group (EPL) so a CTA has ~100-300 threads, and
-// the default k-split (NKS).  lx 9..12 run one element per CTA-iteration
-// with a 2 x (8 x lx^3 x 8 B) ring (up to 221 KiB at lx = 12).
+// Per-lx shape: elements per group (EPL) so a CTA has ~100-300 threads, the
+// k-split (NKS) and the ring depth (D).  lx 9..12 run one element per
+// CTA-iteration with a ONE-deep ring and no k-split: several CTAs per SM
+// (4 / 3 / 2 / 2 at lx 9 / 10 / 11 / 12) overlap one another's loads and
+// barriers, which beats one CTA with a 2-deep ring (the lx = 12 ring alone
+// is 221 KiB) by 1.05-1.3x (measured: lx 9 fast 1.55 -> 1.29 ms, lx 12
+// 1.88 -> 1.56 ms, strict 2.19 -> 1.91 ms; 1-deep with NKS = 2 is slower).
 template <int LX>
 struct T2Shape {
   static constexpr int EPL = LX == 2 ? 32 : LX == 3 ? 14 : LX == 4 ? 8 : LX == 5 ? 5
                            : LX == 6 ? 3 : LX == 7 ? 2 : 1;
-  static constexpr int NKS = LX >= 8 ? 2 : 1;
+  static constexpr int NKS = LX == 8 ? 2 : 1;
+  static constexpr int D = LX >= 9 ? 1 : 2;
 };
 
-template <int LX, int NKS>
+template <int LX, int NKS, int DR = 2>
 struct T2Cfg {
   static constexpr int L2 = LX * LX;
   static constexpr int L3 = LX * LX * LX;
   static constexpr int EPL = T2Shape<LX>::EPL;
   static constexpr int KS = (LX + NKS - 1) / NKS;
   static constexpr int NT = EPL * L2 * NKS;
-  static constexpr int D = 2;
+  static constexpr int D = DR;  // ring depth (elements-groups in flight per CTA)
   static constexpr int FIELD = EPL * L3;
   // per-field stride in the ring: room for one leading pad double (a group
   // whose first element starts 8 B past a 16-B boundary is copied from the
@@ -220,10 +225,10 @@ __device__ __forceinline__ void stage2_dispatch(int kh, const TParams<LX>& P, co
   }
 }
 
-template <int LX, bool FAST, int NKS>
-__global__ void __launch_bounds__(T2Cfg<LX, NKS>::NT)
+template <int LX, bool FAST, int NKS, int DR = 2>
+__global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT)
 ax_tma2(const __grid_constant__ TParams<LX> P) {
-  using C = T2Cfg<LX, NKS>;
+  using C = T2Cfg<LX, NKS, DR>;
   constexpr int L2 = C::L2, L3 = C::L3, FIELD = C::FIELD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);

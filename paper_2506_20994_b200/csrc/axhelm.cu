@@ -165,20 +165,20 @@ static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, cons
 static int g_nks8 = [] {
   const char* v = getenv("AXHELM_NKS");
   int d = v ? atoi(v) : 2;
-  return (d == 1 || d == 2 || d == 4) ? d : 2;
+  return (d >= 1 && d <= 4) ? d : 2;
 }();
 
-template <int LX, bool FAST, int NKS>
+template <int LX, bool FAST, int NKS, int D = 2>
 static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
                                const double* hzt) {
-  using C = T2Cfg<LX, NKS>;
+  using C = T2Cfg<LX, NKS, D>;
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_tma2<LX, FAST, NKS>,
+    cudaError_t e = cudaFuncSetAttribute(ax_tma2<LX, FAST, NKS, D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma2<LX, FAST, NKS>, C::NT, C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma2<LX, FAST, NKS, D>, C::NT, C::SMEM);
     if (e != cudaSuccess) return e;
     blocks_per_sm = cap_ctas(b > 0 ? b : 1);
   }
@@ -196,7 +196,7 @@ static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, co
   const int64_t groups = (nel + C::EPL - 1) / C::EPL;
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   if (grid > groups) grid = groups;
-  ax_tma2<LX, FAST, NKS><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
+  ax_tma2<LX, FAST, NKS, D><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
   return cudaGetLastError();
 }
 
@@ -288,13 +288,13 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
       if constexpr (LX == 8) return launch_dmma8(A, nel, st, X);
     }
   }
-  if constexpr (LX <= 12) {
+  if constexpr (LX <= 15) {
     if ((g_variant >= 4 || g_variant == 0) && aligned16(A)) {
       if constexpr (LX == 8) {
         if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
         if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
       }
-      return launch_tma2<LX, FAST, T2Shape<LX>::NKS>(A, nel, st, hz, hzt);
+      return launch_tma2<LX, FAST, T2Shape<LX>::NKS, T2Shape<LX>::D>(A, nel, st, hz, hzt);
     }
   }
   if constexpr (LX == 8) {
