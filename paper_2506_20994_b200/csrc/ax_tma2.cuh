@@ -48,6 +48,9 @@ struct T2Shape {
                            : LX == 6 ? 3 : LX == 7 ? 2 : 1;
   static constexpr int NKS = LX == 8 ? 2 : 1;
   static constexpr int D = LX >= 9 ? 1 : 2;
+  // split issue of the next group (issue_group2_part): measured 1.05-1.07x
+  // at lx 13 / 15, 0.94-0.87x at lx 10 / 12 (where it changes the schedule)
+  static constexpr bool SPLIT = LX >= 13;
 };
 
 template <int LX, int NKS, int DR = 2>
@@ -91,6 +94,36 @@ __device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_
 #pragma unroll
   for (int f = 0; f < 8; ++f) bulk_g2s(buf + f * C::FSTRIDE, field_ptr(A, f) + lo, bytes, bar);
   return pad;
+}
+
+// Split issue for the one-deep ring (NKS = 1, ut in registers): the fields
+// stage 2 does not read (u, h1, g33, g12, g13, g23) are re-filled for the
+// next group as soon as stage 1 is done (PART 0: arrive + expect all 8
+// fields' bytes, 6 copies), g11 / g22 (holding ur / us) after stage 2
+// (PART 1: 2 copies completing the same barrier phase).
+template <int LX, int NKS, int PART>
+__device__ __forceinline__ void issue_group2_part(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
+                                                  uint64_t* bar) {
+  using C = T2Cfg<LX, NKS>;
+  const int64_t e0 = g * C::EPL;
+  const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
+  const int64_t first = e0 * C::L3, last = (e0 + ne) * C::L3;
+  const int pad = (int)(first & 1);
+  const int64_t lo = first - pad, hi = (last + 1) & ~(int64_t)1;
+  if (hi > nel * C::L3) {  // fallback group (cooperative load by the consumer)
+    if (PART == 0) mbar_arrive(bar);
+    return;
+  }
+  const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+  if (PART == 0) {
+    mbar_arrive_expect_tx(bar, 8u * bytes);
+#pragma unroll
+    for (int f = 0; f < 8; ++f)
+      if (f != 2 && f != 3) bulk_g2s(buf + f * C::FSTRIDE, field_ptr(A, f) + lo, bytes, bar);
+  } else {
+    bulk_g2s(buf + 2 * C::FSTRIDE, field_ptr(A, 2) + lo, bytes, bar);
+    bulk_g2s(buf + 3 * C::FSTRIDE, field_ptr(A, 3) + lo, bytes, bar);
+  }
 }
 
 // matrix entry source: kernel parameters (constant bank) or shared memory
@@ -310,20 +343,24 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
     ElemView v{buf + 0 * FS + eoff, buf + 1 * FS + eoff, buf + 2 * FS + eoff,
                buf + 3 * FS + eoff, buf + 4 * FS + eoff, buf + 5 * FS + eoff,
                buf + 6 * FS + eoff, buf + 7 * FS + eoff};
+    constexpr bool SPLIT = C::D == 1 && NKS == 1 && T2Shape<LX>::SPLIT;
+    const int64_t gn = g + C::D * stride;
     double utr[LX];
     if (use_param) stage1_dispatch<LX, FAST, NKS, true>(kh, P, sZ, v, dxr, dyr, j, i, utr);
     else stage1_dispatch<LX, FAST, NKS, false>(kh, P, sZ, v, dxr, dyr, j, i, utr);
     __syncthreads();  // ur / us / ut of the whole element visible
+    if (SPLIT && tid == 0 && gn < ngroups) {
+      fence_proxy_async();
+      issue_group2_part<LX, NKS, 0>(A, nel, gn, buf, &bars[b]);
+    }
     double* wout = A.w + (e0 + el) * L3 + p;
     if (use_param) stage2_dispatch<LX, FAST, NKS, true>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
     else stage2_dispatch<LX, FAST, NKS, false>(kh, P, sZt, v, dxtr, dytr, j, i, utr, wout, active);
     __syncthreads();  // every read of buffer b is done
-    if (tid == 0) {
-      const int64_t gn = g + C::D * stride;
-      if (gn < ngroups) {
-        fence_proxy_async();
-        issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
-      }
+    if (tid == 0 && gn < ngroups) {
+      fence_proxy_async();
+      if constexpr (SPLIT) issue_group2_part<LX, NKS, 1>(A, nel, gn, buf, &bars[b]);
+      else issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
     }
   }
 }
