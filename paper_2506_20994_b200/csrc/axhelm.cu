@@ -294,6 +294,9 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
         if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
         if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
       }
+      // lx = 7 strict: the one-deep ring (5 CTAs per SM instead of 2) is 1.08x
+      // faster; for fast mode and lx 4..6 the two depths are within noise
+      if constexpr (LX == 7 && !FAST) return launch_tma2<LX, FAST, 1, 1>(A, nel, st, hz, hzt);
       return launch_tma2<LX, FAST, T2Shape<LX>::NKS, T2Shape<LX>::D>(A, nel, st, hz, hzt);
     }
   }
