@@ -246,8 +246,9 @@ def kernel_name(lx, mode):
     if v == "auto":
         if lx == 8 and mode == "fast":
             return "ax_dmma8 (FP64 DMMA m8n8k4, TMA ring)"
-        if lx <= 12:
-            return f"ax_tma2<{lx},{mode}> (TMA ring, FP64 vector)"
+        if lx <= 15:
+            ring = "one-deep" if lx >= 9 or (lx == 7 and mode == "strict") else "two-deep"
+            return f"ax_tma2<{lx},{mode}> (TMA ring {ring}, FP64 vector)"
         return f"ax_kwalk_pf<{lx},{mode}> (L2-prefetch k-walk)"
     return f"AXHELM_KERNEL={v}"
 

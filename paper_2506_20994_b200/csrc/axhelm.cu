@@ -67,7 +67,7 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
 // pf (v2, L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
 // + k-split) or dmma (v6, FP64 tensor cores; fast mode, lx = 8).  Default
-// ("auto"): v6 for fast lx = 8, v4 for every other lx <= 12 (16-B aligned
+// ("auto"): v6 for fast lx = 8, v4 for every other lx <= 15 (16-B aligned
 // fields), else v2.  (v3 = v4 without its refinements and v5 = row per
 // thread were measured and retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
