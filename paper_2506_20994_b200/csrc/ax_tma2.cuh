@@ -51,7 +51,25 @@ struct T2Shape {
   // split issue of the next group (issue_group2_part): measured 1.05-1.07x
   // at lx 13 / 15, 0.94-0.87x at lx 10 / 12 (where it changes the schedule)
   static constexpr bool SPLIT = LX >= 13;
+  // one-deep ring: also L2-prefetch the group after the one being loaded
+  // (bytes in flight beyond what shared memory holds)
+  static constexpr bool PF = LX >= 9;
 };
+
+// L2 prefetch of field f of elements [e0, e0 + ne) (16-B aligned interior)
+template <int LX>
+__device__ __forceinline__ void prefetch_elems(const AxPtrs& A, int64_t e0, int64_t ne, int f) {
+  constexpr int64_t L3 = (int64_t)LX * LX * LX;
+  uintptr_t lo = (uintptr_t)(field_ptr(A, f) + e0 * L3);
+  uintptr_t hi = (uintptr_t)(field_ptr(A, f) + (e0 + ne) * L3);
+  lo = (lo + 15) & ~(uintptr_t)15;
+  hi = hi & ~(uintptr_t)15;
+  while (hi > lo) {
+    const uint32_t n = (uint32_t)((hi - lo) > 65536 ? 65536 : (hi - lo));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const void*)lo), "r"(n) : "memory");
+    lo += n;
+  }
+}
 
 template <int LX, int NKS, int DR = 2>
 struct T2Cfg {
@@ -361,6 +379,13 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
       fence_proxy_async();
       if constexpr (SPLIT) issue_group2_part<LX, NKS, 1>(A, nel, gn, buf, &bars[b]);
       else issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
+    }
+    if constexpr (T2Shape<LX>::PF && C::D == 1) {
+      const int64_t gp = gn + stride;
+      if (tid < 8 && gp < ngroups) {
+        const int64_t ep = gp * C::EPL;
+        prefetch_elems<LX>(A, ep, (nel - ep < C::EPL) ? nel - ep : C::EPL, tid);
+      }
     }
   }
 }
