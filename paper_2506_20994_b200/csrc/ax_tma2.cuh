@@ -24,6 +24,11 @@
 
 #include "ax_tma.cuh"
 
+// L2 prefetch distance (groups beyond the one being loaded) of the one-deep ring
+#ifndef AXB_PFD
+#define AXB_PFD 1
+#endif
+
 namespace axb {
 
 template <int LX>
@@ -53,7 +58,7 @@ struct T2Shape {
   static constexpr bool SPLIT = LX >= 13;
   // one-deep ring: also L2-prefetch the group after the one being loaded
   // (bytes in flight beyond what shared memory holds)
-  static constexpr bool PF = LX >= 9;
+  static constexpr int PF = LX >= 9 ? AXB_PFD : 0;
 };
 
 // L2 prefetch of field f of elements [e0, e0 + ne) (16-B aligned interior)
@@ -380,8 +385,8 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
       if constexpr (SPLIT) issue_group2_part<LX, NKS, 1>(A, nel, gn, buf, &bars[b]);
       else issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
     }
-    if constexpr (T2Shape<LX>::PF && C::D == 1) {
-      const int64_t gp = gn + stride;
+    if constexpr (T2Shape<LX>::PF > 0 && C::D == 1) {
+      const int64_t gp = gn + T2Shape<LX>::PF * stride;
       if (tid < 8 && gp < ngroups) {
         const int64_t ep = gp * C::EPL;
         prefetch_elems<LX>(A, ep, (nel - ep < C::EPL) ? nel - ep : C::EPL, tid);
