@@ -301,6 +301,19 @@ def mesh_dims(nel):
     return 1, 1, nel
 
 
+def pick_exchange(args, comm, torch, device, ws):
+    """Interface-plane transport for N > 1: "peer" (the plane kernels write the
+    neighbours' buffers over NVLink, dist.PeerExchange) when every rank's GPU
+    can reach every other's, else "nccl"; --exchange forces one."""
+    if ws == 1:
+        return "nccl"
+    if args.exchange != "auto":
+        return args.exchange
+    devs = comm.allgather_object(device.index)
+    ok = all(d == device.index or torch.cuda.can_device_access_peer(device.index, d) for d in devs)
+    return "peer" if all(comm.allgather_object(ok)) else "nccl"
+
+
 def ours_arm(args):
     import torch
 
@@ -330,8 +343,24 @@ def ours_arm(args):
     nx, ny, nzr = mesh_dims(nel)
     mesh = BoxMesh(nx, ny, nzr * ws, lx, rank, ws)
     assert mesh.nel == nel
-    op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1,
-                           schedule=args.gs_schedule if not args.gs_schedule.isdigit() else int(args.gs_schedule))
+    sched = args.gs_schedule if not args.gs_schedule.isdigit() else int(args.gs_schedule)
+    xchg = pick_exchange(args, comm, torch, device, ws)
+    op = None
+    if xchg == "peer":
+        try:
+            op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1, schedule=sched,
+                                   exchange="peer")
+            ok = True
+        except Exception as exc:  # noqa: BLE001 - any setup failure -> NCCL on every rank
+            print(f"bench: peer exchange unavailable ({exc}); using NCCL", file=sys.stderr)
+            ok = False
+        if not all(comm.allgather_object(ok)):
+            if op is not None and op.peer is not None:
+                comm.dist.barrier()
+                op.peer.close()
+            op, xchg = None, "nccl"
+    if op is None:
+        op = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, amp=0.1, schedule=sched)
     g = torch.Generator(device=device).manual_seed(1234 + rank)
     u = torch.randn(mesh.shape, dtype=torch.float64, device=device, generator=g)
     w = torch.empty_like(u)
@@ -420,7 +449,7 @@ def ours_arm(args):
         g_ms = g_total / args.gs_steps
         # the concurrent-follower schedule for comparison (DSSUM on w in L2)
         op0 = HelmholtzOperator(mesh, torch, device, comm=comm, mode=args.mode, geometry=op.geom,
-                                schedule="follow")
+                                schedule="follow")  # NCCL transport: no second IPC region
         u0_total, _, _ = timed_fn(lambda: op0.apply(u, w), args.gs_steps, 3, False)
         u0_ms = u0_total / args.gs_steps
         del op0
@@ -431,8 +460,11 @@ def ours_arm(args):
                    "dssum_ms": round(g_ms - total_ms / args.steps, 5),
                    "schedule": {-1: "follow", 0: "sequential"}.get(op.schedule, op.schedule),
                    "follow_schedule_ms_per_step": round(u0_ms, 5),
-                   "exchange": ("NCCL P2P planes, overlapped with interior ax" if ws > 1 and not
-                                comm.host_staged else ("gloo host-staged planes" if ws > 1 else "none (1 rank)")),
+                   "exchange": ("none (1 rank)" if ws == 1 else
+                                "peer memory: plane kernels write the neighbours' buffers (CUDA IPC / NVLink), "
+                                "overlapped with interior ax" if op.peer is not None else
+                                "gloo host-staged planes" if comm.host_staged else
+                                "NCCL P2P planes, overlapped with interior ax"),
                    "plane_bytes": mesh.plane * 8}
 
     # ---- Jacobi-PCG, 100 iterations  [C5 per GPU]
@@ -473,9 +505,16 @@ def ours_arm(args):
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_leg(args, lib)
 
-    if rank != 0:
+    def teardown():
         if ws > 1:
+            torch.cuda.synchronize()
+            torch.distributed.barrier()  # no rank frees its peer region while a neighbour may write it
+            if op.peer is not None:
+                op.peer.close()
             torch.distributed.destroy_process_group()
+
+    if rank != 0:
+        teardown()
         return
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
@@ -507,8 +546,7 @@ def ours_arm(args):
         "ax_plus_gs": gs_line, "pcg": cg_line,
     }
     print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    teardown()
 
 
 def e2e_leg(args, torch, lib, arr, device):
@@ -581,6 +619,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gs", action="store_true", help="skip the ax + DSSUM measurement")
     ap.add_argument("--gs-steps", type=int, default=50)
+    ap.add_argument("--exchange", choices=("auto", "nccl", "peer"), default="auto",
+                    help="interface-plane transport for N > 1 (auto: peer if every GPU pair has P2P)")
     ap.add_argument("--gs-schedule", default="sequential",
                     help="ax + DSSUM schedule: follow | sequential | <layers per block>")
     ap.add_argument("--no-cg", action="store_true", help="skip the Jacobi-PCG measurement")

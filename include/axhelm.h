@@ -147,6 +147,25 @@ int axhelm_gs_box(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_
 int axhelm_gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
                         int64_t zlo, int64_t zhi, void* stream);
 
+/* Peer-memory interface exchange (multi-GPU DSSUM without NCCL): device
+ * allocations shared between the ranks' processes with CUDA IPC (64-byte
+ * cudaIpcMemHandle), and the interface-plane steps writing the neighbour's
+ * receive buffer / flag directly over NVLink.  op AXHELM_GS_PARTIAL: top
+ * plane partial sums -> out (upper rank's buffer), then signal_flag = seq;
+ * AXHELM_GS_FINISH: wait *wait_flag >= seq, continue from in (own buffer),
+ * write the bottom-plane copies, final sums -> out (lower rank's buffer),
+ * signal; AXHELM_GS_WRITE: wait, write the top-plane copies from in.
+ * counter: a zeroed unsigned in local device memory per op.  Same
+ * summation order as axhelm_gs_box ops 1..3 (bit-identical). */
+int axhelm_peer_alloc(int64_t bytes, void** ptr, void* handle);
+int axhelm_peer_open(const void* handle, void** ptr);
+int axhelm_peer_close(void* ptr);
+int axhelm_peer_free(void* ptr);
+int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                       const double* in, double* out, const unsigned long long* wait_flag,
+                       unsigned long long* signal_flag, unsigned long long seq, unsigned* counter,
+                       void* stream);
+
 /* Assembled local operator on a BoxMesh slab: ax_helm on the slab's local
  * element layers [l0, l1) and the local DSSUM of the owned node planes
  * [zlo, zhi] (layers outside [l0, l1) must already be applied, stream-

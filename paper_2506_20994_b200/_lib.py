@@ -36,6 +36,13 @@ PROTOTYPES = {
     "axhelm_gs_box_range": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp]),
     "axhelm_reduce_blocks": (ctypes.c_int, [ctypes.c_int64]),
+    "axhelm_peer_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p), _vp]),
+    "axhelm_peer_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "axhelm_peer_close": (ctypes.c_int, [_vp]),
+    "axhelm_peer_free": (ctypes.c_int, [_vp]),
+    "axhelm_gs_box_peer": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp,
+                                           ctypes.c_ulonglong, _vp, _vp]),
     "axhelm_ax_gs_box": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int] * 3 + [ctypes.c_int64] * 6
                          + [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "axhelm_ax_gs_scratch": (ctypes.c_int, [ctypes.c_int64]),

@@ -22,6 +22,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "../../include/axhelm.h"
 #include "ax_launch.h"
@@ -251,7 +252,7 @@ namespace axb {
 // 2 = FINISH (continue from buf, write back, sum -> buf), 3 = WRITE (buf -> copies).
 template <int LX, int OP>
 __device__ __forceinline__ void gs_box_node(double* __restrict__ w, const BoxGS& M, int gx, int gy,
-                                            int gz, double* __restrict__ buf) {
+                                            int gz, const double* in, double* out) {
   constexpr int n1 = LX - 1;
   constexpr int L3 = LX * LX * LX;
   constexpr int64_t DX = L3 - n1;
@@ -268,7 +269,7 @@ __device__ __forceinline__ void gs_box_node(double* __restrict__ w, const BoxGS&
     ok[c] = dz < cz && dy < cy && dx < cx;
     off[c] = off0 + dx * DX + dy * DY + dz * DZ;
   }
-  double s = (OP == 2 || OP == 3) ? buf[slot] : 0.0;
+  double s = (OP == 2 || OP == 3) ? in[slot] : 0.0;
   if (OP != 3) {
     double v[8];
 #pragma unroll
@@ -278,13 +279,13 @@ __device__ __forceinline__ void gs_box_node(double* __restrict__ w, const BoxGS&
       if (ok[c]) s = __dadd_rn(s, v[c]);
   }
   if (OP == 1) {
-    buf[slot] = s;
+    out[slot] = s;
     return;
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (ok[c]) w[off[c]] = s;
-  if (OP == 2) buf[slot] = s;
+  if (OP == 2) out[slot] = s;
 }
 
 // Interface-plane steps: one thread per node of plane gz (x fastest).
@@ -293,7 +294,60 @@ __global__ void gs_box_plane_kernel(double* __restrict__ w, const BoxGS M, int g
                                     double* __restrict__ buf) {
   const int gx = blockIdx.x * blockDim.x + threadIdx.x;
   if (gx >= M.NX) return;
-  gs_box_node<LX, OP>(w, M, gx, blockIdx.y, gz, buf);
+  gs_box_node<LX, OP>(w, M, gx, blockIdx.y, gz, buf, buf);
+}
+
+__device__ __forceinline__ unsigned long long peer_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The same interface-plane steps with the neighbour's buffers in PEER memory
+// (CUDA IPC over NVLink): the exchange is done by the kernels themselves, no
+// NCCL and no host synchronisation.
+//   PARTIAL (top plane)   : out = upper rank's receive buffer; signal its flag
+//   FINISH  (bottom plane): wait own flag >= seq; in = own receive buffer
+//                           (the lower rank's partials); out = lower rank's
+//                           receive buffer; signal its flag
+//   WRITE   (top plane)   : wait own flag >= seq; in = own receive buffer
+// Signal: every CTA fences at system scope after its stores and counts
+// itself in; the last one publishes seq with a system-scope release store.
+// Wait: thread 0 of every CTA spins on an acquire load (10 s -> __trap()).
+template <int LX, int OP>
+__global__ void gs_box_plane_peer_kernel(double* __restrict__ w, const BoxGS M, int gz,
+                                         const double* in, double* out,
+                                         const unsigned long long* wait_flag,
+                                         unsigned long long* signal_flag, unsigned long long seq,
+                                         unsigned* counter) {
+  if (OP >= 2) {
+    if (threadIdx.x == 0) {
+      unsigned long long v = 0, t0 = 0;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(wait_flag) : "memory");
+        if (v >= seq) break;
+        __nanosleep(128);
+        const unsigned long long t = peer_timer();
+        if (t0 == 0) t0 = t;
+        if (t - t0 > 10000000000ull) __trap();
+      }
+    }
+    __syncthreads();
+  }
+  const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gx < M.NX) gs_box_node<LX, OP>(w, M, gx, blockIdx.y, gz, in, out);
+  if (OP <= 2) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(counter, 1u) == total - 1) {
+        *counter = 0;
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(signal_flag), "l"(seq) : "memory");
+      }
+    }
+  }
 }
 
 // Local DSSUM, enumerating only (potentially) shared nodes, densely:
@@ -694,4 +748,65 @@ extern "C" int axhelm_gs_box_range(double* w, int nx, int ny, int lx, int64_t ez
     return set_status(AXHELM_EINVAL, "axhelm_gs_box_range: %s", why);
   return cuda_status(axb::gs_box_range(w, nx, ny, lx, ez0, ez1, zlo, zhi, (cudaStream_t)stream),
                      "axhelm_gs_box_range");
+}
+
+// ------------------------------------------------------------ peer memory
+// IPC-shareable device allocations for the peer-memory interface exchange
+// (dist.PeerExchange): allocated and zeroed here, exported as a 64-byte
+// cudaIpcMemHandle, opened by the neighbouring ranks (NVLink peer mapping).
+extern "C" int axhelm_peer_alloc(int64_t bytes, void** ptr, void* handle) {
+  if (bytes <= 0 || !ptr || !handle) return set_status(AXHELM_EINVAL, "axhelm_peer_alloc: bad arguments");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), *ptr);
+  return cuda_status(e, "axhelm_peer_alloc");
+}
+
+extern "C" int axhelm_peer_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return set_status(AXHELM_EINVAL, "axhelm_peer_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "axhelm_peer_open");
+}
+
+extern "C" int axhelm_peer_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr), "axhelm_peer_close"); }
+
+extern "C" int axhelm_peer_free(void* ptr) { return cuda_status(cudaFree(ptr), "axhelm_peer_free"); }
+
+// One interface-plane step of the structured DSSUM with peer buffers
+// (op = AXHELM_GS_PARTIAL / _FINISH / _WRITE, see gs_box_plane_peer_kernel).
+extern "C" int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
+                                  const double* in, double* out, const unsigned long long* wait_flag,
+                                  unsigned long long* signal_flag, unsigned long long seq,
+                                  unsigned* counter, void* stream) {
+  if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez1 <= ez0 || ez0 < 0)
+    return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: bad sizes");
+  if (op < 0 || op > 2) return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: unknown op %d", op);
+  if ((op != AXHELM_GS_WRITE && (!out || !signal_flag || !counter)) ||
+      (op != AXHELM_GS_PARTIAL && (!in || !wait_flag)))
+    return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: missing buffer for op %d", op);
+  const int n1 = lx - 1;
+  BoxGS M{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1};
+  if (M.NY > 65535) return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: mesh too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 blk(128), grd((unsigned)((M.NX + 127) / 128), (unsigned)M.NY, 1);
+  const int gz = (int)((op == AXHELM_GS_FINISH ? ez0 : ez1) * n1);
+  switch (lx) {
+#define AXB_PEER(N)                                                                                       \
+  case N:                                                                                                 \
+    if (op == AXHELM_GS_PARTIAL)                                                                          \
+      axb::gs_box_plane_peer_kernel<N, 1><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
+                                                               seq, counter);                             \
+    else if (op == AXHELM_GS_FINISH)                                                                      \
+      axb::gs_box_plane_peer_kernel<N, 2><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
+                                                               seq, counter);                             \
+    else                                                                                                  \
+      axb::gs_box_plane_peer_kernel<N, 3><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
+                                                               seq, counter);                             \
+    break;
+    AXB_PEER(2) AXB_PEER(3) AXB_PEER(4) AXB_PEER(5) AXB_PEER(6) AXB_PEER(7) AXB_PEER(8) AXB_PEER(9)
+    AXB_PEER(10) AXB_PEER(11) AXB_PEER(12) AXB_PEER(13) AXB_PEER(14) AXB_PEER(15) AXB_PEER(16)
+#undef AXB_PEER
+  }
+  return cuda_status(cudaGetLastError(), "axhelm_gs_box_peer");
 }

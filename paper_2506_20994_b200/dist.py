@@ -24,6 +24,8 @@ oracle-backed ops (tests/test_dist_cpu.py).
 
 from __future__ import annotations
 
+import ctypes
+
 from .gs import FINISH, PARTIAL, WRITE
 
 
@@ -59,6 +61,11 @@ class TorchComm:
         if self.host_staged and recv is not None and r_t is not recv:
             recv.copy_(r_t)
 
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
     def allreduce_sum(self, t):
         if self.host_staged and t.device.type != "cpu":
             h = t.cpu()
@@ -67,6 +74,97 @@ class TorchComm:
             return t
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return t
+
+
+class PeerExchange:
+    """The interface-plane exchange over PEER memory: each rank
+    exports one IPC-shareable device region (receive buffers for the planes
+    from below / above and the flags its neighbours signal) and opens its
+    neighbours' regions; the plane kernels (axhelm_gs_box_peer) write the
+    partial / final sums straight into the neighbour's buffer over NVLink and
+    signal with a system-scope release store.  No NCCL, no host round trip:
+    one apply's exchange is three kernel launches on the caller's stream.
+
+      rank r:  PARTIAL top plane  -> recv_bot of r+1, flag_bot(r+1) = seq
+               FINISH bottom plane (waits flag_bot(r) >= seq)
+                                  -> recv_top of r-1, flag_top(r-1) = seq
+               WRITE top plane     (waits flag_top(r) >= seq)
+
+    Summation order = the NCCL path's (bit-identical).  Works between
+    processes on different GPUs (NVLink peer mappings) and on one GPU."""
+
+    HEAD = 512  # flags (0: from below, 8: from above), counters at 256 / 260
+
+    def __init__(self, mesh, comm, lib, torch=None):
+        self.mesh = mesh
+        self.lib = lib
+        self.rank, self.world = comm.rank, comm.world
+        self.has_top = self.rank < self.world - 1
+        self.has_bot = self.rank > 0
+        self.plane_bytes = ((mesh.plane * 8 + 255) // 256) * 256
+        size = self.HEAD + 2 * self.plane_bytes
+        self.base = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        self._check(lib.axhelm_peer_alloc(size, ctypes.byref(self.base), handle))
+        handles = comm.allgather_object(bytes(handle))
+        self.peer_bot = self._open(handles[self.rank - 1]) if self.has_bot else None
+        self.peer_top = self._open(handles[self.rank + 1]) if self.has_top else None
+        self.seq = 0
+
+    def _check(self, rc):
+        if rc:
+            from . import _lib
+            from .errors import DeviceError
+
+            raise DeviceError(_lib.last_error(self.lib))
+
+    def _open(self, handle: bytes):
+        p = ctypes.c_void_p()
+        buf = (ctypes.c_char * 64).from_buffer_copy(handle)
+        self._check(self.lib.axhelm_peer_open(buf, ctypes.byref(p)))
+        return p.value
+
+    # region layout
+    @staticmethod
+    def _flag_bot(b):
+        return b
+    @staticmethod
+    def _flag_top(b):
+        return b + 8
+
+    def _recv_bot(self, b):
+        return b + self.HEAD
+
+    def _recv_top(self, b):
+        return b + self.HEAD + self.plane_bytes
+
+    def exchange(self, w, stream):
+        """Interface planes of w (this rank's slab), stream-ordered."""
+        m = self.mesh
+        self.seq += 1
+        b = self.base.value
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        args = (m.nx, m.ny, m.lx, m.ez0, m.ez1)
+        if self.has_top:
+            self._check(self.lib.axhelm_gs_box_peer(PARTIAL, w.data_ptr(), *args, None,
+                                                    self._recv_bot(self.peer_top), None,
+                                                    self._flag_bot(self.peer_top), self.seq, b + 256, sp))
+        if self.has_bot:
+            self._check(self.lib.axhelm_gs_box_peer(FINISH, w.data_ptr(), *args, self._recv_bot(b),
+                                                    self._recv_top(self.peer_bot), self._flag_bot(b),
+                                                    self._flag_top(self.peer_bot), self.seq, b + 260, sp))
+        if self.has_top:
+            self._check(self.lib.axhelm_gs_box_peer(WRITE, w.data_ptr(), *args, self._recv_top(b), None,
+                                                    self._flag_top(b), None, self.seq, None, sp))
+
+    def close(self):
+        for p in (self.peer_bot, self.peer_top):
+            if p:
+                self.lib.axhelm_peer_close(ctypes.c_void_p(p))
+        self.peer_bot = self.peer_top = None
+        if self.base:
+            self.lib.axhelm_peer_free(self.base)
+            self.base = ctypes.c_void_p()
 
 
 class SlabDSSUM:

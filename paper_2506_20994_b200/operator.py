@@ -45,7 +45,7 @@ class HelmholtzOperator:
 
     def __init__(self, mesh: BoxMesh, torch, device, comm=None, mode: str = "fast",
                  geometry: dict | None = None, amp: float = 0.1, overlap: bool = True,
-                 schedule: str | int = "sequential"):
+                 schedule: str | int = "sequential", exchange: str = "nccl"):
         self.mesh = mesh
         self.torch = torch
         self.device = device
@@ -72,6 +72,16 @@ class HelmholtzOperator:
         self.zlo = mesh.ez0 * n1 + (1 if mesh.rank > 0 else 0)
         self.zhi = mesh.ez1 * n1 - (1 if mesh.rank < mesh.world - 1 else 0)
         self._progress = torch.zeros(max(nl, 1), dtype=torch.int32, device=device)
+        # interface-plane transport: "nccl" (TorchComm send/recv of plane
+        # buffers) or "peer" (dist.PeerExchange: the plane kernels write the
+        # neighbour's buffers over NVLink themselves)
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
+        self.peer = None
+        if exchange == "peer" and comm is not None and mesh.world > 1:
+            from .dist import PeerExchange
+
+            self.peer = PeerExchange(mesh, comm, self.lib)
 
     # ----------------------------------------------------------- pieces
 
@@ -173,6 +183,9 @@ class HelmholtzOperator:
         send down -> WRITE (top).  Touches only interface-plane points."""
         m = self.mesh
         d = self.dssum
+        if self.peer is not None:
+            self.peer.exchange(w, self.torch.cuda.current_stream(self.device))
+            return
         if d.has_top:
             self.gs.plane(0, "top", w, d.buf_top)
         if m.world > 1:

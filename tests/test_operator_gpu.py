@@ -97,7 +97,7 @@ def _free_port():
     return p
 
 
-def _rank_worker(rank, world, port, dims, mode, block, q):
+def _rank_worker(rank, world, port, dims, mode, block, q, exchange="nccl", applies=1):
     import torch
     import torch.distributed as dist
 
@@ -111,27 +111,37 @@ def _rank_worker(rank, world, port, dims, mode, block, q):
 
         nx, ny, nz, lx = dims
         m = BoxMesh(nx, ny, nz, lx, rank, world)
-        op = HelmholtzOperator(m, torch, "cuda", comm=TorchComm(dist), mode=mode, schedule=block)
+        op = HelmholtzOperator(m, torch, "cuda", comm=TorchComm(dist), mode=mode, schedule=block,
+                               exchange=exchange)
         ug = np.random.default_rng(5).standard_normal((nx * ny * nz, lx, lx, lx))
         u = torch.from_numpy(ug[m.ez0 * nx * ny: m.ez1 * nx * ny].copy()).cuda()
         w = torch.empty_like(u)
         d = torch.zeros(1, dtype=torch.float64, device="cuda")
-        op.apply(u, w, dot=d)
+        for _ in range(applies):  # repeated applies: the peer flags' sequence numbers advance
+            w.fill_(np.nan)
+            op.apply(u, w, dot=d)
         torch.cuda.synchronize()
         q.put((rank, w.cpu().numpy(), float(d), op.overlap))
+        if op.peer is not None:
+            dist.barrier()  # nobody frees its region while a neighbour may still write it
+            op.peer.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,dims,block", [("strict", (3, 2, 8, 5), "sequential"),
-                                             ("strict", (3, 2, 8, 5), "follow"),
-                                             ("strict", (3, 2, 8, 5), 2),
-                                             ("fast", (2, 3, 8, 8), "follow")])
-def test_two_ranks_on_one_gpu_bit_exact(torch, mode, dims, block):
+@pytest.mark.parametrize("mode,dims,block,exchange", [("strict", (3, 2, 8, 5), "sequential", "nccl"),
+                                                      ("strict", (3, 2, 8, 5), "follow", "nccl"),
+                                                      ("strict", (3, 2, 8, 5), 2, "nccl"),
+                                                      ("fast", (2, 3, 8, 8), "follow", "nccl"),
+                                                      ("strict", (3, 2, 8, 5), "sequential", "peer"),
+                                                      ("fast", (2, 3, 8, 8), "sequential", "peer")])
+def test_two_ranks_on_one_gpu_bit_exact(torch, mode, dims, block, exchange):
     """z-slab ranks with the overlapped boundary/interior apply and the
-    interface exchange (gloo, host-staged): the gathered result equals the
+    interface exchange — host-staged over gloo ("nccl" transport path) or
+    through peer memory (CUDA IPC between the two processes, the kernels
+    writing each other's buffers and flags) — the gathered result equals the
     single-domain sequential apply bit for bit (and, in strict mode, the
-    oracle) for every schedule."""
+    oracle) for every schedule, over three consecutive applies."""
     import torch.multiprocessing as mp
 
     from paper_2506_20994_b200.mesh import BoxMesh
@@ -142,7 +152,7 @@ def test_two_ranks_on_one_gpu_bit_exact(torch, mode, dims, block):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, dims, mode, block, q))
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, dims, mode, block, q, exchange, 3))
              for r in range(world)]
     for p in procs:
         p.start()
