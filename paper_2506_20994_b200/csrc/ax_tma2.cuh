@@ -59,6 +59,8 @@ struct T2Shape {
   // one-deep ring: also L2-prefetch the group after the one being loaded
   // (bytes in flight beyond what shared memory holds)
   static constexpr int PF = LX >= 9 ? AXB_PFD : 0;
+  // minimum resident CTAs per SM handed to ptxas (register cap); 1 = none
+  static constexpr int MINB = LX == 10 ? 3 : 1;
 };
 
 // L2 prefetch of field f of elements [e0, e0 + ne) (16-B aligned interior)
@@ -282,7 +284,7 @@ __device__ __forceinline__ void stage2_dispatch(int kh, const TParams<LX>& P, co
 }
 
 template <int LX, bool FAST, int NKS, int DR = 2>
-__global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT)
+__global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT, (DR == 1 ? T2Shape<LX>::MINB : 1))
 ax_tma2(const __grid_constant__ TParams<LX> P) {
   using C = T2Cfg<LX, NKS, DR>;
   constexpr int L2 = C::L2, L3 = C::L3, FIELD = C::FIELD;
