@@ -60,7 +60,13 @@ struct T2Shape {
   // (bytes in flight beyond what shared memory holds)
   static constexpr int PF = LX >= 9 ? AXB_PFD : 0;
   // minimum resident CTAs per SM handed to ptxas (register cap); 1 = none
-  static constexpr int MINB = LX == 10 ? 3 : 1;  // lx = 7 with 5: spills, 1.07x slower
+  // ptxas minimum-blocks hint of the one-deep ring (register budget): 0 =
+  // none (ptxas heuristics, 168 registers at lx 9..12), 1 = up to 255, n =
+  // 65536 / (n threads).  Measured A/B on one box: lx 10 -> 3 (3 CTAs per
+  // SM: fast 1.50 -> 1.29 ms), lx 11 -> 1 (strict 1.92 -> 1.72 ms), lx 12
+  // -> 0 (255 registers would leave 1 CTA per SM: 1.56 -> 2.0 ms); lx 7
+  // with 5: spills, 1.07x slower.
+  static constexpr int MINB = LX == 10 ? 3 : (LX == 11 ? 1 : 0);  // lx 9 -> 1: 1.27 -> 1.69 ms
 };
 
 // L2 prefetch of field f of elements [e0, e0 + ne) (16-B aligned interior)
@@ -85,12 +91,13 @@ struct T2Cfg {
   static constexpr int EPL = T2Shape<LX>::EPL;
   static constexpr int KS = (LX + NKS - 1) / NKS;
   static constexpr int NT = EPL * L2 * NKS;
-  static constexpr int D = DR;  // ring depth (elements-groups in flight per CTA)
+  static constexpr int D = DR;  // ring depth (element groups in flight per CTA)
   static constexpr int FIELD = EPL * L3;
   // per-field stride in the ring: room for one leading pad double (a group
   // whose first element starts 8 B past a 16-B boundary is copied from the
   // aligned address below it) and 16-B alignment of every field
   static constexpr int FSTRIDE = (FIELD + 2 + 1) & ~1;
+  static constexpr int MINB = D == 1 ? T2Shape<LX>::MINB : 0;
   static constexpr int BUF = 8 * FSTRIDE;
   static constexpr size_t SMEM = 128 + sizeof(double) * (D * BUF + 2 * L2);
 };
@@ -101,10 +108,10 @@ struct T2Cfg {
 // `pad` (0 or 1) doubles into the field's slot.  A superset that would read
 // past the end of the arrays (last group, odd total) falls back to a plain
 // arrive + cooperative load.  Returns pad, or -1 for the fallback.
-template <int LX, int NKS>
+template <int LX, int NKS, int DR = 2>
 __device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
                                             uint64_t* bar) {
-  using C = T2Cfg<LX, NKS>;
+  using C = T2Cfg<LX, NKS, DR>;
   const int64_t e0 = g * C::EPL;
   const int64_t ne = (nel - e0 < C::EPL) ? nel - e0 : C::EPL;
   const int64_t first = e0 * C::L3, last = (e0 + ne) * C::L3;  // doubles
@@ -126,7 +133,7 @@ __device__ __forceinline__ int issue_group2(const AxPtrs& A, int64_t nel, int64_
 // next group as soon as stage 1 is done (PART 0: arrive + expect all 8
 // fields' bytes, 6 copies), g11 / g22 (holding ur / us) after stage 2
 // (PART 1: 2 copies completing the same barrier phase).
-template <int LX, int NKS, int PART>
+template <int LX, int NKS, int PART, int DR = 2>
 __device__ __forceinline__ void issue_group2_part(const AxPtrs& A, int64_t nel, int64_t g, double* buf,
                                                   uint64_t* bar) {
   using C = T2Cfg<LX, NKS>;
@@ -284,7 +291,7 @@ __device__ __forceinline__ void stage2_dispatch(int kh, const TParams<LX>& P, co
 }
 
 template <int LX, bool FAST, int NKS, int DR = 2>
-__global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT, (DR == 1 ? T2Shape<LX>::MINB : 1))
+__global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT, T2Cfg<LX, NKS, DR>::MINB)
 ax_tma2(const __grid_constant__ TParams<LX> P) {
   using C = T2Cfg<LX, NKS, DR>;
   constexpr int L2 = C::L2, L3 = C::L3, FIELD = C::FIELD;
@@ -318,7 +325,7 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
 #pragma unroll
     for (int d = 0; d < C::D; ++d) {
       const int64_t g = blockIdx.x + d * stride;
-      if (g < ngroups) issue_group2<LX, NKS>(A, nel, g, bufs + d * C::BUF, &bars[d]);
+      if (g < ngroups) issue_group2<LX, NKS, DR>(A, nel, g, bufs + d * C::BUF, &bars[d]);
     }
   }
   // device copy of the t-direction matrices (transposed) + verification of
@@ -385,7 +392,7 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
     if (tid == 0 && gn < ngroups) {
       fence_proxy_async();
       if constexpr (SPLIT) issue_group2_part<LX, NKS, 1>(A, nel, gn, buf, &bars[b]);
-      else issue_group2<LX, NKS>(A, nel, gn, buf, &bars[b]);
+      else issue_group2<LX, NKS, DR>(A, nel, gn, buf, &bars[b]);
     }
     if constexpr (T2Shape<LX>::PF > 0 && C::D == 1) {
       const int64_t gp = gn + T2Shape<LX>::PF * stride;
