@@ -67,6 +67,9 @@ struct T2Shape {
   // -> 0 (255 registers would leave 1 CTA per SM: 1.56 -> 2.0 ms); lx 7
   // with 5: spills, 1.07x slower.
   static constexpr int MINB = LX == 10 ? 3 : (LX == 11 ? 1 : 0);  // lx 9 -> 1: 1.27 -> 1.69 ms
+  // the same hint for the two-deep ring: 1 (up to 255 registers) measured
+  // 1.01-1.05x at lx 5..7, neutral at lx 2..4, 0.97x at lx = 8 strict
+  static constexpr int MINB2 = (LX >= 5 && LX <= 7) ? 1 : 0;
 };
 
 // L2 prefetch of field f of elements [e0, e0 + ne) (16-B aligned interior)
@@ -97,7 +100,7 @@ struct T2Cfg {
   // whose first element starts 8 B past a 16-B boundary is copied from the
   // aligned address below it) and 16-B alignment of every field
   static constexpr int FSTRIDE = (FIELD + 2 + 1) & ~1;
-  static constexpr int MINB = D == 1 ? T2Shape<LX>::MINB : 0;
+  static constexpr int MINB = D == 1 ? T2Shape<LX>::MINB : T2Shape<LX>::MINB2;
   static constexpr int BUF = 8 * FSTRIDE;
   static constexpr size_t SMEM = 128 + sizeof(double) * (D * BUF + 2 * L2);
 };
