@@ -237,3 +237,17 @@ def test_fast_large_lx_ring_reuse(torch, kern, lx):
         got = run_dev(torch, kern["fast"], arrays, nel, lx)
         assert np.isfinite(got).all(), (lx, nel)
         assert o.normwise_rel(got, o.ax(arrays)) <= FAST_TOL, (lx, nel)
+
+
+def test_mdg_bench_sweep_on_gpu(tmp_path):
+    """tools/mdg_bench: the reference's bench protocol with gpu variants on a
+    small grid; gpu-strict's checksum is the oracle's (bit-exact), gpu-fast
+    passes the relaxed-fp gate."""
+    from tools import mdg_bench
+
+    recs = mdg_bench.run((3, 4), meshes=(128, 256), max_nel=256, reps=3, log=None)
+    assert len(recs) == 2 * 2 * 2
+    assert {r["variant"] for r in recs} == {"gpu-strict", "gpu-fast"}
+    assert all(r["seconds_median"] > 0 and r["gflops"] > 0 for r in recs)
+    text = mdg_bench.render_csv(recs)
+    assert text.splitlines()[0] == mdg_bench.CSV_HEADER and len(text.splitlines()) == 9
