@@ -53,9 +53,11 @@ struct T2Shape {
                            : LX == 6 ? 3 : LX == 7 ? 2 : 1;
   static constexpr int NKS = LX == 8 ? 2 : 1;
   static constexpr int D = LX >= 9 ? 1 : 2;
-  // split issue of the next group (issue_group2_part): measured 1.05-1.07x
-  // at lx 13 / 15, 0.94-0.87x at lx 10 / 12 (where it changes the schedule)
-  static constexpr bool SPLIT = LX >= 13;
+  // split issue of the next group (issue_group2_part), per mode from same-box
+  // A/B: fast 1.03x at lx 9 / 11 / 12, 0.96x at lx 10; strict 1.05-1.07x at
+  // lx 13 / 15, 0.92x at lx 9, neutral at 11 / 12
+  static constexpr bool SPLIT_FAST = LX == 9 || LX >= 11;
+  static constexpr bool SPLIT_STRICT = LX >= 13;
   // one-deep ring: also L2-prefetch the group after the one being loaded
   // (bytes in flight beyond what shared memory holds)
   static constexpr int PF = LX >= 9 ? AXB_PFD : 0;
@@ -378,7 +380,8 @@ ax_tma2(const __grid_constant__ TParams<LX> P) {
     ElemView v{buf + 0 * FS + eoff, buf + 1 * FS + eoff, buf + 2 * FS + eoff,
                buf + 3 * FS + eoff, buf + 4 * FS + eoff, buf + 5 * FS + eoff,
                buf + 6 * FS + eoff, buf + 7 * FS + eoff};
-    constexpr bool SPLIT = C::D == 1 && NKS == 1 && T2Shape<LX>::SPLIT;
+    constexpr bool SPLIT =
+        C::D == 1 && NKS == 1 && (FAST ? T2Shape<LX>::SPLIT_FAST : T2Shape<LX>::SPLIT_STRICT);
     const int64_t gn = g + C::D * stride;
     double utr[LX];
     if (use_param) stage1_dispatch<LX, FAST, NKS, true>(kh, P, sZ, v, dxr, dyr, j, i, utr);
