@@ -794,6 +794,12 @@ extern "C" int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int
   switch (lx) {
 #define AXB_PEER(N)                                                                                       \
   case N:                                                                                                 \
+    /* waiting CTAs must not pin an SM to an L1-heavy carveout the apply's */                            \
+    /* persistent CTAs (running concurrently on another stream) cannot use */                            \
+    cudaFuncSetAttribute(axb::gs_box_plane_peer_kernel<N, 2>,                                             \
+                         cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared); \
+    cudaFuncSetAttribute(axb::gs_box_plane_peer_kernel<N, 3>,                                             \
+                         cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared); \
     if (op == AXHELM_GS_PARTIAL)                                                                          \
       axb::gs_box_plane_peer_kernel<N, 1><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
                                                                seq, counter);                             \
