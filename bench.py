@@ -458,6 +458,9 @@ def ours_arm(args):
                    "steps": args.gs_steps, "ms_per_step": round(g_ms, 5),
                    "gdof_s": round(pts * ws / (g_ms * 1e-3) / 1e9, 4),
                    "dssum_ms": round(g_ms - total_ms / args.steps, 5),
+                   # every 32-B sector of w holds a face point: a separate DSSUM
+                   # pass must read and write all of w (16 B/point) at best
+                   "dssum_floor_ms": round(16 * pts / (measured_peaks()[0] * 1e9) * 1e3, 5),
                    "schedule": {-1: "follow", 0: "sequential"}.get(op.schedule, op.schedule),
                    "follow_schedule_ms_per_step": round(u0_ms, 5),
                    "exchange": ("none (1 rank)" if ws == 1 else
