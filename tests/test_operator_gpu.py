@@ -129,13 +129,14 @@ def _rank_worker(rank, world, port, dims, mode, block, q, exchange="nccl", appli
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,dims,block,exchange", [("strict", (3, 2, 8, 5), "sequential", "nccl"),
-                                                      ("strict", (3, 2, 8, 5), "follow", "nccl"),
-                                                      ("strict", (3, 2, 8, 5), 2, "nccl"),
-                                                      ("fast", (2, 3, 8, 8), "follow", "nccl"),
-                                                      ("strict", (3, 2, 8, 5), "sequential", "peer"),
-                                                      ("fast", (2, 3, 8, 8), "sequential", "peer")])
-def test_two_ranks_on_one_gpu_bit_exact(torch, mode, dims, block, exchange):
+@pytest.mark.parametrize("mode,dims,block,exchange,world", [("strict", (3, 2, 8, 5), "sequential", "nccl", 2),
+                                                            ("strict", (3, 2, 8, 5), "follow", "nccl", 2),
+                                                            ("strict", (3, 2, 8, 5), 2, "nccl", 2),
+                                                            ("fast", (2, 3, 8, 8), "follow", "nccl", 2),
+                                                            ("strict", (3, 2, 8, 5), "sequential", "peer", 2),
+                                                            ("fast", (2, 3, 8, 8), "sequential", "peer", 2),
+                                                            ("strict", (2, 2, 9, 4), "sequential", "peer", 3)])
+def test_ranks_on_one_gpu_bit_exact(torch, mode, dims, block, exchange, world):
     """z-slab ranks with the overlapped boundary/interior apply and the
     interface exchange — host-staged over gloo ("nccl" transport path) or
     through peer memory (CUDA IPC between the two processes, the kernels
@@ -148,7 +149,6 @@ def test_two_ranks_on_one_gpu_bit_exact(torch, mode, dims, block, exchange):
     from paper_2506_20994_b200.operator import HelmholtzOperator
 
     nx, ny, nz, lx = dims
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
