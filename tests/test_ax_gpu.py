@@ -251,3 +251,57 @@ def test_mdg_bench_sweep_on_gpu(tmp_path):
     assert all(r["seconds_median"] > 0 and r["gflops"] > 0 for r in recs)
     text = mdg_bench.render_csv(recs)
     assert text.splitlines()[0] == mdg_bench.CSV_HEADER and len(text.splitlines()) == 9
+
+
+@pytest.mark.parametrize("lx,nel", [(8, 1 << 18), (12, 57870), (5, 800000)])
+def test_full_size_operator_properties(torch, kern, lx, nel):
+    """Size-independent properties of A at the sweep / C2 sizes, both modes
+    (tests/test_oracle.py:129-135, :175-185, :227-231 restated per element):
+    symmetry <v, A u> = <u, A v>, the constant null space A 1 = 0, positive
+    semi-definiteness <u, A u> >= 0, and fast == strict to 1e-12 normwise."""
+    from paper_2506_20994_b200 import gll_basis
+
+    g = torch.Generator(device="cuda").manual_seed(lx)
+    shape = (nel, lx, lx, lx)
+    f64 = dict(dtype=torch.float64, device="cuda")
+    # SPD metric per point: M M^T + 0.1 I (the reference's distribution)
+    m = [torch.rand(shape, generator=g, **f64) * 2 - 1 for _ in range(9)]
+
+    def dot(a, c):
+        return m[3 * a] * m[3 * c] + m[3 * a + 1] * m[3 * c + 1] + m[3 * a + 2] * m[3 * c + 2]
+
+    dev = {"g11d": dot(0, 0) + 0.1, "g22d": dot(1, 1) + 0.1, "g33d": dot(2, 2) + 0.1,
+           "g12d": dot(0, 1), "g13d": dot(0, 2), "g23d": dot(1, 2),
+           "h1d": torch.rand(shape, generator=g, **f64) + 0.5}
+    del m
+    a, b = gll_basis(lx).operator_matrices()
+    for n in ("dxd", "dyd", "dzd"):
+        dev[n] = torch.from_numpy(a).cuda()
+    for n in ("dxtd", "dytd", "dztd"):
+        dev[n] = torch.from_numpy(b).cuda()
+    u = torch.randn(shape, generator=g, **f64)
+    v = torch.randn(shape, generator=g, **f64)
+
+    def apply(mode, x):
+        dev["ud"] = x
+        dev["wd"] = torch.empty(shape, **f64)
+        kern[mode](dev, nel, lx)
+        return dev["wd"]
+
+    res = {}
+    for mode in ("strict", "fast"):
+        au, av = apply(mode, u), apply(mode, v)
+        vau = (v * au).sum(dim=(1, 2, 3))
+        uav = (u * av).sum(dim=(1, 2, 3))
+        scale = ((v.abs() * au.abs()).sum(dim=(1, 2, 3)) + (u.abs() * av.abs()).sum(dim=(1, 2, 3)))
+        assert float(((vau - uav).abs() / scale).max()) <= 1e-13, mode
+        uau = (u * au).sum(dim=(1, 2, 3))
+        assert float((uau / (u.abs() * au.abs()).sum(dim=(1, 2, 3))).min()) >= -1e-13, mode
+        one = apply(mode, torch.ones(shape, **f64))
+        # relative to the operator's typical output (rounding of the D rows'
+        # cancellation grows with lx and max|D| ~ lx^2 / 4)
+        assert float(one.abs().max()) <= 1e-12 * float(au.abs().max()), mode
+        res[mode] = au
+    torch.cuda.synchronize()
+    err = float((res["fast"] - res["strict"]).abs().max() / res["strict"].abs().max())
+    assert err <= FAST_TOL
