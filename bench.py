@@ -491,7 +491,10 @@ def ours_arm(args):
         cg_line = {"iters": args.cg_iters, "ms_total": round(c_ms, 3),
                    "ms_per_iter": round(c_ms / args.cg_iters, 5),
                    "gdof_s_per_iter": round(pts * ws * args.cg_iters / (c_ms * 1e-3) / 1e9, 4),
-                   "rr_reduction": float(h[-1] / h[0])}
+                   "rr_reduction": float(h[-1] / h[0]),
+                   "allreduce": ("none (1 rank)" if ws == 1 else
+                                 "peer memory (axhelm_peer_allreduce)" if op.peer is not None else
+                                 "gloo host-staged" if comm.host_staged else "NCCL")}
         del pcg, f
 
     ms_step = total_ms / args.steps

@@ -165,6 +165,14 @@ int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, i
                        const double* in, double* out, const unsigned long long* wait_flag,
                        unsigned long long* signal_flag, unsigned long long seq, unsigned* counter,
                        void* stream);
+/* All-reduce (sum) of n <= 4 doubles over `world` ranks through peer
+ * memory: bases = device array of every rank's peer region (own included),
+ * each reserving axhelm_peer_allreduce_bytes() at byte offset `off`; seq
+ * increases by one per call on every rank.  The sum is taken in rank order,
+ * so every rank gets the same bits.  v may alias out. */
+int64_t axhelm_peer_allreduce_bytes(void);
+int axhelm_peer_allreduce(const double* v, int n, double* out, const unsigned long long* bases,
+                          int64_t off, int world, int rank, unsigned long long seq, void* stream);
 
 /* Assembled local operator on a BoxMesh slab: ax_helm on the slab's local
  * element layers [l0, l1) and the local DSSUM of the owned node planes

@@ -40,6 +40,9 @@ PROTOTYPES = {
     "axhelm_peer_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
     "axhelm_peer_close": (ctypes.c_int, [_vp]),
     "axhelm_peer_free": (ctypes.c_int, [_vp]),
+    "axhelm_peer_allreduce_bytes": (ctypes.c_int64, []),
+    "axhelm_peer_allreduce": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int64, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_ulonglong, _vp]),
     "axhelm_gs_box_peer": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp,
                                            ctypes.c_ulonglong, _vp, _vp]),

@@ -96,7 +96,10 @@ class JacobiPCG:
 
     def _allreduce(self, t):
         if self.op.comm is not None and self.op.mesh.world > 1:
-            self.op.comm.allreduce_sum(t)
+            if self.op.peer is not None:  # through peer memory, no NCCL
+                self.op.peer.allreduce_sum(t)
+            else:
+                self.op.comm.allreduce_sum(t)
 
     def solve(self, f, iters: int = 100):
         """Run `iters` PCG iterations from x = 0.  Returns (x, rr_history)

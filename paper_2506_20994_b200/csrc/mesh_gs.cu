@@ -816,3 +816,68 @@ extern "C" int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int
   }
   return cuda_status(cudaGetLastError(), "axhelm_gs_box_peer");
 }
+
+// ------------------------------------------------------- peer all-reduce
+// Sum of a few doubles over all ranks through peer memory (PCG's dot
+// products): every rank writes its values into slot [parity][rank] of every
+// rank's region (bases[q] + off) and raises flag [rank] there with a
+// system-scope release store; then waits until all its flags reach seq and
+// sums the slots in rank order — the same bits on every rank, no NCCL.
+// Two parity buffers: a rank can run at most one call ahead of another
+// rank's read (its next call needs that rank's next write).
+namespace axb {
+constexpr int PEER_MAXW = 64;
+__global__ void peer_allreduce_kernel(const double* v, int n, double* out,
+                                      const unsigned long long* __restrict__ bases, int64_t off,
+                                      int world, int rank, unsigned long long seq) {
+  const int t = threadIdx.x;
+  const int par = (int)(seq & 1);
+  double val[4];
+  for (int j = 0; j < 4; ++j) val[j] = j < n ? v[j] : 0.0;
+  if (t < world) {  // write my values to rank t, then raise its flag [rank]
+    unsigned char* b = reinterpret_cast<unsigned char*>(bases[t]) + off;
+    unsigned long long* flags = reinterpret_cast<unsigned long long*>(b);
+    double* data = reinterpret_cast<double*>(b + 8 * PEER_MAXW) + ((size_t)par * PEER_MAXW + rank) * 4;
+    for (int j = 0; j < n; ++j) data[j] = val[j];
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags + rank), "l"(seq) : "memory");
+  }
+  __syncthreads();
+  unsigned char* mine = reinterpret_cast<unsigned char*>(bases[rank]) + off;
+  if (t < world) {  // wait for rank t's values in my region
+    const unsigned long long* f = reinterpret_cast<const unsigned long long*>(mine) + t;
+    unsigned long long x = 0, t0 = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+      if (x >= seq) break;
+      __nanosleep(64);
+      const unsigned long long now = peer_timer();
+      if (t0 == 0) t0 = now;
+      if (now - t0 > 10000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double* data = reinterpret_cast<const double*>(mine + 8 * PEER_MAXW) + (size_t)par * PEER_MAXW * 4;
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int q = 0; q < world; ++q) s += data[q * 4 + j];
+      out[j] = s;
+    }
+  }
+}
+}  // namespace axb
+
+// bytes of the all-reduce area a peer region must reserve at `off`
+extern "C" int64_t axhelm_peer_allreduce_bytes(void) {
+  return 8 * axb::PEER_MAXW + 2 * axb::PEER_MAXW * 4 * 8;
+}
+
+extern "C" int axhelm_peer_allreduce(const double* v, int n, double* out, const unsigned long long* bases,
+                                     int64_t off, int world, int rank, unsigned long long seq, void* stream) {
+  if (n < 1 || n > 4 || world < 1 || world > axb::PEER_MAXW || rank < 0 || rank >= world || !v || !out ||
+      !bases)
+    return set_status(AXHELM_EINVAL, "axhelm_peer_allreduce: bad arguments");
+  axb::peer_allreduce_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(v, n, out, bases, off, world, rank, seq);
+  return cuda_status(cudaGetLastError(), "axhelm_peer_allreduce");
+}

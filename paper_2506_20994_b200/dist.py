@@ -91,25 +91,49 @@ class PeerExchange:
                WRITE top plane     (waits flag_top(r) >= seq)
 
     Summation order = the NCCL path's (bit-identical).  Works between
-    processes on different GPUs (NVLink peer mappings) and on one GPU."""
+    processes on different GPUs (NVLink peer mappings) and on one GPU.
+
+    The same regions carry the PCG's small all-reduces (`allreduce_sum`):
+    each rank writes its values into every rank's region and sums the slots
+    in rank order (axhelm_peer_allreduce) — identical bits on every rank."""
 
     HEAD = 512  # flags (0: from below, 8: from above), counters at 256 / 260
 
     def __init__(self, mesh, comm, lib, torch=None):
+        import torch as _torch
+
         self.mesh = mesh
         self.lib = lib
         self.rank, self.world = comm.rank, comm.world
         self.has_top = self.rank < self.world - 1
         self.has_bot = self.rank > 0
         self.plane_bytes = ((mesh.plane * 8 + 255) // 256) * 256
-        size = self.HEAD + 2 * self.plane_bytes
+        self.ar_off = self.HEAD + 2 * self.plane_bytes
+        size = self.ar_off + lib.axhelm_peer_allreduce_bytes()
         self.base = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
         self._check(lib.axhelm_peer_alloc(size, ctypes.byref(self.base), handle))
         handles = comm.allgather_object(bytes(handle))
-        self.peer_bot = self._open(handles[self.rank - 1]) if self.has_bot else None
-        self.peer_top = self._open(handles[self.rank + 1]) if self.has_top else None
+        self.peers = {q: (self._open(h) if q != self.rank else self.base.value) for q, h in enumerate(handles)}
+        self.peer_bot = self.peers[self.rank - 1] if self.has_bot else None
+        self.peer_top = self.peers[self.rank + 1] if self.has_top else None
+        dev = _torch.device("cuda", _torch.cuda.current_device())
+        self.bases = _torch.tensor([self.peers[q] for q in range(self.world)], dtype=_torch.int64, device=dev)
         self.seq = 0
+        self.ar_seq = 0
+
+    def allreduce_sum(self, t):
+        """In-place sum of a small float64 device tensor (<= 4 values) over all
+        ranks, on the current stream."""
+        import torch as _torch
+
+        assert t.dtype == _torch.float64 and t.is_contiguous() and t.numel() <= 4
+        self.ar_seq += 1
+        stream = _torch.cuda.current_stream()
+        self._check(self.lib.axhelm_peer_allreduce(t.data_ptr(), t.numel(), t.data_ptr(), self.bases.data_ptr(),
+                                                   self.ar_off, self.world, self.rank, self.ar_seq,
+                                                   ctypes.c_void_p(stream.cuda_stream)))
+        return t
 
     def _check(self, rc):
         if rc:
@@ -158,9 +182,10 @@ class PeerExchange:
                                                     self._flag_top(b), None, self.seq, None, sp))
 
     def close(self):
-        for p in (self.peer_bot, self.peer_top):
-            if p:
+        for q, p in getattr(self, "peers", {}).items():
+            if q != self.rank and p:
                 self.lib.axhelm_peer_close(ctypes.c_void_p(p))
+        self.peers = {}
         self.peer_bot = self.peer_top = None
         if self.base:
             self.lib.axhelm_peer_free(self.base)

@@ -92,3 +92,82 @@ def test_fused_update_matches_separate_passes(torch, dims, mode):
     torch.cuda.synchronize()
     assert float(((h1 - h2).abs() / h2).max()) <= 1e-10
     assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-10
+
+
+def _pcg_rank_worker(rank, world, port, dims, exchange, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_20994_b200.cg import JacobiPCG
+        from paper_2506_20994_b200.dist import TorchComm
+        from paper_2506_20994_b200.mesh import BoxMesh
+        from paper_2506_20994_b200.operator import HelmholtzOperator
+
+        nx, ny, nz, lx = dims
+        m = BoxMesh(nx, ny, nz, lx, rank, world)
+        op = HelmholtzOperator(m, torch, "cuda", comm=TorchComm(dist), mode="strict", exchange=exchange)
+        pcg = JacobiPCG(op)
+        gid = m.gid(torch, "cuda")
+        fg = torch.from_numpy(np.random.default_rng(2).standard_normal(
+            (nx * (lx - 1) + 1) * (ny * (lx - 1) + 1) * (nz * (lx - 1) + 1))).cuda()
+        x, hist = pcg.solve(fg[gid], iters=15)
+        torch.cuda.synchronize()
+        q.put((rank, x.cpu().numpy(), hist.cpu().numpy()))
+        dist.barrier()
+        if op.peer is not None:
+            op.peer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange,world", [("nccl", 2), ("peer", 2), ("peer", 3)])
+def test_pcg_ranks_on_one_gpu(torch, exchange, world):
+    """Multi-rank PCG (z-slabs, ranks sharing one GPU): the interface exchange
+    and the dot all-reduces through gloo ("nccl" transport path) or through
+    peer memory (CUDA IPC; axhelm_gs_box_peer + axhelm_peer_allreduce).  The
+    iterates match the single-domain solve to reassociation of the dots, and
+    with the peer all-reduce every rank holds the same residual history bit
+    for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2506_20994_b200.mesh import BoxMesh
+
+    dims = (2, 3, 9, 4)
+    nx, ny, nz, lx = dims
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pcg_rank_worker, args=(r, world, port, dims, exchange, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, x, h = q.get(timeout=300)
+        res[r] = (x, h)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m, op, pcg = _setup(torch, nx, ny, nz, lx, "strict")
+    gid = m.gid(torch, "cuda")
+    fg = torch.from_numpy(np.random.default_rng(2).standard_normal(
+        (nx * (lx - 1) + 1) * (ny * (lx - 1) + 1) * (nz * (lx - 1) + 1))).cuda()
+    xw, hw = pcg.solve(fg[gid], iters=15)
+    hw = hw.cpu().numpy()
+    for r in range(world):
+        assert np.max(np.abs(res[r][1] - hw) / hw) <= 1e-10, r
+    x = np.concatenate([res[r][0] for r in range(world)])
+    assert o.normwise_rel(x, xw.cpu().numpy()) <= 1e-10
+    if exchange == "peer":
+        for r in range(1, world):
+            assert np.array_equal(res[r][1], res[0][1])
