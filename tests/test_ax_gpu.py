@@ -305,3 +305,19 @@ def test_full_size_operator_properties(torch, kern, lx, nel):
     torch.cuda.synchronize()
     err = float((res["fast"] - res["strict"]).abs().max() / res["strict"].abs().max())
     assert err <= FAST_TOL
+
+
+def test_pageable_host_path_large_bit_exact(torch, kern):
+    """Ordinary (pageable) NumPy buffers through __dace_ax_helm's staged path
+    (host copy threads -> pinned slots -> device, several chunks in flight):
+    bit-identical to the device-buffer apply."""
+    lx, nel = 8, 9000  # 4.6 Mi points: more than one 1 Mi-point chunk per slot cycle
+    arrays = o.problem(lx, nel, seed=5)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
+    kern["strict"](dev, nel, lx)
+    torch.cuda.synchronize()
+    want = dev["wd"].cpu().numpy()
+    host = {k: np.ascontiguousarray(v).copy() for k, v in arrays.items()}
+    host["wd"][:] = np.nan
+    kern["strict"](host, nel, lx)
+    assert np.array_equal(host["wd"], want)

@@ -15,11 +15,12 @@ from paper_2506_20994_b200 import _lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--mode", default="fast")
+ap.add_argument("--pageable", action="store_true", help="ordinary (pageable) host memory, as a numpy caller passes")
 a = ap.parse_args()
 lib = _lib.load()
 nel, lx = 1 << 18, 8
 arr = bench.device_problem(torch, nel, lx, torch.device("cuda", 0))
-host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in arr.items()}
+host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=not a.pageable) for k, v in arr.items()}
 for k, v in arr.items():
     host[k].copy_(v)
 del arr
@@ -34,4 +35,4 @@ for _ in range(a.reps):
     ts.append(time.perf_counter() - t0)
 t = min(ts)
 h2d = sum(host[n].numel() * 8 for n in bench.ABI if n != "wd")
-print(f"e2e {t * 1e3:.1f} ms  {nel * lx ** 3 / t / 1e9:.3f} GDOF/s  H2D {h2d / t / 1e9:.1f} GB/s", flush=True)
+print(f"e2e ({'pageable' if a.pageable else 'pinned'}) {t * 1e3:.1f} ms  {nel * lx ** 3 / t / 1e9:.3f} GDOF/s  H2D {h2d / t / 1e9:.1f} GB/s", flush=True)
