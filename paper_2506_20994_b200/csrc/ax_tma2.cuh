@@ -60,7 +60,9 @@ struct T2Shape {
   static constexpr bool SPLIT_STRICT = LX >= 13;
   // one-deep ring: also L2-prefetch the group after the one being loaded
   // (bytes in flight beyond what shared memory holds)
-  static constexpr int PF = LX >= 9 ? AXB_PFD : 0;
+  // (one-deep ring at lx >= 9 and the lx = 7 strict path: 1.07x there;
+  // the same prefetch in the two-deep ring measured 0.8-0.97x at lx 3..8)
+  static constexpr int PF = LX >= 9 || LX == 7 ? AXB_PFD : 0;
   // minimum resident CTAs per SM handed to ptxas (register cap); 1 = none
   // ptxas minimum-blocks hint of the one-deep ring (register budget): 0 =
   // none (ptxas heuristics, 168 registers at lx 9..12), 1 = up to 255, n =
