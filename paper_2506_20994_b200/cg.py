@@ -101,9 +101,37 @@ class JacobiPCG:
             else:
                 self.op.comm.allreduce_sum(t)
 
-    def solve(self, f, iters: int = 100):
+    def solve(self, f, iters: int = 100, graph: bool = False):
         """Run `iters` PCG iterations from x = 0.  Returns (x, rr_history)
-        where rr_history[i] = <r_i, r_i> (device tensor, i = 0..iters)."""
+        where rr_history[i] = <r_i, r_i> (device tensor, i = 0..iters).
+
+        graph=True (single rank): the whole solve — init and `iters`
+        iterations, ~10 kernels each — is captured once into a CUDA graph
+        (per f and iters) and replayed: one launch instead of ~10 iters, for
+        problems small enough to be launch-bound.  Same kernels, same
+        results bit for bit."""
+        if graph:
+            return self._solve_graph(f, iters)
+        return self._solve(f, iters)
+
+    def _solve_graph(self, f, iters):
+        torch = self.torch
+        if self.op.mesh.world > 1:
+            raise ValueError("graph=True needs a single rank (the exchanges synchronise with peers)")
+        key = (f.data_ptr(), iters)
+        cache = self.__dict__.setdefault("_graphs", {})
+        if key not in cache:
+            self._solve(f, 1)  # warm-up: one-time library setup (attributes, matrix caches)
+            torch.cuda.synchronize(self.op.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                out = self._solve(f, iters)
+            cache[key] = (g, out)
+        g, out = cache[key]
+        g.replay()
+        return out
+
+    def _solve(self, f, iters):
         torch = self.torch
         dev = self.op.device
         n = self.n

@@ -171,3 +171,19 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
     if exchange == "peer":
         for r in range(1, world):
             assert np.array_equal(res[r][1], res[0][1])
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_graph_replay_equals_eager(torch, mode):
+    """The CUDA-graph PCG (whole solve captured once, replayed) gives the
+    eager solve's iterates bit for bit, on repeated replays."""
+    m, op, pcg = _setup(torch, 3, 2, 2, 8, mode)
+    gid = m.gid(torch, "cuda")
+    f = torch.randn(int(gid.max()) + 1, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(9))[gid].contiguous()
+    xe, he = pcg.solve(f, iters=20)
+    xe, he = xe.clone(), he.clone()
+    for _ in range(2):
+        xg, hg = pcg.solve(f, iters=20, graph=True)
+        torch.cuda.synchronize()
+        assert torch.equal(hg, he) and torch.equal(xg, xe)
