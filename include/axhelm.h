@@ -164,7 +164,11 @@ int axhelm_peer_free(void* ptr);
 int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
                        const double* in, double* out, const unsigned long long* wait_flag,
                        unsigned long long* signal_flag, unsigned long long seq, unsigned* counter,
-                       void* stream);
+                       const unsigned long long* seq_dev, void* stream);
+/* seq_dev (nullable): take the sequence number as *seq_dev + 1 on the device
+ * instead of `seq` (so a captured CUDA graph advances it on every replay);
+ * axhelm_peer_seq_bump increments it after one exchange's steps. */
+int axhelm_peer_seq_bump(unsigned long long* seq_dev, void* stream);
 /* All-reduce (sum) of n <= 4 doubles over `world` ranks through peer
  * memory: bases = device array of every rank's peer region (own included),
  * each reserving axhelm_peer_allreduce_bytes() at byte offset `off`; seq
@@ -172,7 +176,8 @@ int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, i
  * so every rank gets the same bits.  v may alias out. */
 int64_t axhelm_peer_allreduce_bytes(void);
 int axhelm_peer_allreduce(const double* v, int n, double* out, const unsigned long long* bases,
-                          int64_t off, int world, int rank, unsigned long long seq, void* stream);
+                          int64_t off, int world, int rank, unsigned long long seq,
+                          unsigned long long* seq_dev, void* stream);  /* seq_dev: as above, bumped here */
 
 /* Assembled local operator on a BoxMesh slab: ax_helm on the slab's local
  * element layers [l0, l1) and the local DSSUM of the owned node planes

@@ -42,10 +42,11 @@ PROTOTYPES = {
     "axhelm_peer_free": (ctypes.c_int, [_vp]),
     "axhelm_peer_allreduce_bytes": (ctypes.c_int64, []),
     "axhelm_peer_allreduce": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int64, ctypes.c_int,
-                                              ctypes.c_int, ctypes.c_ulonglong, _vp]),
+                                              ctypes.c_int, ctypes.c_ulonglong, _vp, _vp]),
     "axhelm_gs_box_peer": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp,
-                                           ctypes.c_ulonglong, _vp, _vp]),
+                                           ctypes.c_ulonglong, _vp, _vp, _vp]),
+    "axhelm_peer_seq_bump": (ctypes.c_int, [_vp, _vp]),
     "axhelm_ax_gs_box": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int] * 3 + [ctypes.c_int64] * 6
                          + [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "axhelm_ax_gs_scratch": (ctypes.c_int, [ctypes.c_int64]),

@@ -105,19 +105,21 @@ class JacobiPCG:
         """Run `iters` PCG iterations from x = 0.  Returns (x, rr_history)
         where rr_history[i] = <r_i, r_i> (device tensor, i = 0..iters).
 
-        graph=True (single rank): the whole solve — init and `iters`
-        iterations, ~10 kernels each — is captured once into a CUDA graph
-        (per f and iters) and replayed: one launch instead of ~10 iters, for
-        problems small enough to be launch-bound.  Same kernels, same
-        results bit for bit."""
+        graph=True: the whole solve — init and `iters` iterations, ~10
+        kernels each — is captured once into a CUDA graph (per f and iters)
+        and replayed: one launch instead of ~10 iters, for problems small
+        enough to be launch-bound.  Same kernels, same results bit for bit.
+        Several ranks: only with the peer-memory exchange, whose sequence
+        numbers live in device memory so every replay advances them."""
         if graph:
             return self._solve_graph(f, iters)
         return self._solve(f, iters)
 
     def _solve_graph(self, f, iters):
         torch = self.torch
-        if self.op.mesh.world > 1:
-            raise ValueError("graph=True needs a single rank (the exchanges synchronise with peers)")
+        if self.op.mesh.world > 1 and self.op.peer is None:
+            raise ValueError("graph=True with several ranks needs the peer-memory exchange "
+                             "(NCCL / gloo calls are not captured)")
         key = (f.data_ptr(), iters)
         cache = self.__dict__.setdefault("_graphs", {})
         if key not in cache:

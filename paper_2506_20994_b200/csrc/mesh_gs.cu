@@ -319,7 +319,8 @@ __global__ void gs_box_plane_peer_kernel(double* __restrict__ w, const BoxGS M, 
                                          const double* in, double* out,
                                          const unsigned long long* wait_flag,
                                          unsigned long long* signal_flag, unsigned long long seq,
-                                         unsigned* counter) {
+                                         unsigned* counter, const unsigned long long* seq_dev) {
+  if (seq_dev) seq = *seq_dev + 1;  // device-side sequence (graph replays advance it)
   if (OP >= 2) {
     if (threadIdx.x == 0) {
       unsigned long long v = 0, t0 = 0;
@@ -775,10 +776,18 @@ extern "C" int axhelm_peer_free(void* ptr) { return cuda_status(cudaFree(ptr), "
 
 // One interface-plane step of the structured DSSUM with peer buffers
 // (op = AXHELM_GS_PARTIAL / _FINISH / _WRITE, see gs_box_plane_peer_kernel).
+__global__ void peer_seq_bump_kernel(unsigned long long* ctr) { *ctr += 1; }
+
+extern "C" int axhelm_peer_seq_bump(unsigned long long* ctr, void* stream) {
+  if (!ctr) return set_status(AXHELM_EINVAL, "axhelm_peer_seq_bump: null counter");
+  peer_seq_bump_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(ctr);
+  return cuda_status(cudaGetLastError(), "axhelm_peer_seq_bump");
+}
+
 extern "C" int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1,
                                   const double* in, double* out, const unsigned long long* wait_flag,
                                   unsigned long long* signal_flag, unsigned long long seq,
-                                  unsigned* counter, void* stream) {
+                                  unsigned* counter, const unsigned long long* seq_dev, void* stream) {
   if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez1 <= ez0 || ez0 < 0)
     return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: bad sizes");
   if (op < 0 || op > 2) return set_status(AXHELM_EINVAL, "axhelm_gs_box_peer: unknown op %d", op);
@@ -802,13 +811,13 @@ extern "C" int axhelm_gs_box_peer(int op, double* w, int nx, int ny, int lx, int
                          cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared); \
     if (op == AXHELM_GS_PARTIAL)                                                                          \
       axb::gs_box_plane_peer_kernel<N, 1><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
-                                                               seq, counter);                             \
+                                                               seq, counter, seq_dev);                    \
     else if (op == AXHELM_GS_FINISH)                                                                      \
       axb::gs_box_plane_peer_kernel<N, 2><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
-                                                               seq, counter);                             \
+                                                               seq, counter, seq_dev);                    \
     else                                                                                                  \
       axb::gs_box_plane_peer_kernel<N, 3><<<grd, blk, 0, st>>>(w, M, gz, in, out, wait_flag, signal_flag, \
-                                                               seq, counter);                             \
+                                                               seq, counter, seq_dev);                    \
     break;
     AXB_PEER(2) AXB_PEER(3) AXB_PEER(4) AXB_PEER(5) AXB_PEER(6) AXB_PEER(7) AXB_PEER(8) AXB_PEER(9)
     AXB_PEER(10) AXB_PEER(11) AXB_PEER(12) AXB_PEER(13) AXB_PEER(14) AXB_PEER(15) AXB_PEER(16)
@@ -829,8 +838,10 @@ namespace axb {
 constexpr int PEER_MAXW = 64;
 __global__ void peer_allreduce_kernel(const double* v, int n, double* out,
                                       const unsigned long long* __restrict__ bases, int64_t off,
-                                      int world, int rank, unsigned long long seq) {
+                                      int world, int rank, unsigned long long seq,
+                                      unsigned long long* seq_dev) {
   const int t = threadIdx.x;
+  if (seq_dev) seq = *seq_dev + 1;  // device-side sequence (graph replays advance it)
   const int par = (int)(seq & 1);
   double val[4];
   for (int j = 0; j < 4; ++j) val[j] = j < n ? v[j] : 0.0;
@@ -864,6 +875,7 @@ __global__ void peer_allreduce_kernel(const double* v, int n, double* out,
       for (int q = 0; q < world; ++q) s += data[q * 4 + j];
       out[j] = s;
     }
+    if (seq_dev) *seq_dev = seq;
   }
 }
 }  // namespace axb
@@ -874,10 +886,12 @@ extern "C" int64_t axhelm_peer_allreduce_bytes(void) {
 }
 
 extern "C" int axhelm_peer_allreduce(const double* v, int n, double* out, const unsigned long long* bases,
-                                     int64_t off, int world, int rank, unsigned long long seq, void* stream) {
+                                     int64_t off, int world, int rank, unsigned long long seq,
+                                     unsigned long long* seq_dev, void* stream) {
   if (n < 1 || n > 4 || world < 1 || world > axb::PEER_MAXW || rank < 0 || rank >= world || !v || !out ||
       !bases)
     return set_status(AXHELM_EINVAL, "axhelm_peer_allreduce: bad arguments");
-  axb::peer_allreduce_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(v, n, out, bases, off, world, rank, seq);
+  axb::peer_allreduce_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(v, n, out, bases, off, world, rank, seq,
+                                                                  seq_dev);
   return cuda_status(cudaGetLastError(), "axhelm_peer_allreduce");
 }

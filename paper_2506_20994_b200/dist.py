@@ -97,7 +97,9 @@ class PeerExchange:
     each rank writes its values into every rank's region and sums the slots
     in rank order (axhelm_peer_allreduce) — identical bits on every rank."""
 
-    HEAD = 512  # flags (0: from below, 8: from above), counters at 256 / 260
+    # region head: flags (0: from below, 8: from above), CTA counters at 256 /
+    # 260, device sequence numbers at 384 (exchange) / 392 (all-reduce)
+    HEAD = 512
 
     def __init__(self, mesh, comm, lib, torch=None):
         import torch as _torch
@@ -131,7 +133,7 @@ class PeerExchange:
         self.ar_seq += 1
         stream = _torch.cuda.current_stream()
         self._check(self.lib.axhelm_peer_allreduce(t.data_ptr(), t.numel(), t.data_ptr(), self.bases.data_ptr(),
-                                                   self.ar_off, self.world, self.rank, self.ar_seq,
+                                                   self.ar_off, self.world, self.rank, 0, self.base.value + 392,
                                                    ctypes.c_void_p(stream.cuda_stream)))
         return t
 
@@ -169,17 +171,19 @@ class PeerExchange:
         b = self.base.value
         sp = ctypes.c_void_p(stream.cuda_stream)
         args = (m.nx, m.ny, m.lx, m.ez0, m.ez1)
+        sq = b + 384  # the sequence lives in device memory: CUDA-graph replays advance it
         if self.has_top:
             self._check(self.lib.axhelm_gs_box_peer(PARTIAL, w.data_ptr(), *args, None,
                                                     self._recv_bot(self.peer_top), None,
-                                                    self._flag_bot(self.peer_top), self.seq, b + 256, sp))
+                                                    self._flag_bot(self.peer_top), 0, b + 256, sq, sp))
         if self.has_bot:
             self._check(self.lib.axhelm_gs_box_peer(FINISH, w.data_ptr(), *args, self._recv_bot(b),
                                                     self._recv_top(self.peer_bot), self._flag_bot(b),
-                                                    self._flag_top(self.peer_bot), self.seq, b + 260, sp))
+                                                    self._flag_top(self.peer_bot), 0, b + 260, sq, sp))
         if self.has_top:
             self._check(self.lib.axhelm_gs_box_peer(WRITE, w.data_ptr(), *args, self._recv_top(b), None,
-                                                    self._flag_top(b), None, self.seq, None, sp))
+                                                    self._flag_top(b), None, 0, None, sq, sp))
+        self._check(self.lib.axhelm_peer_seq_bump(sq, sp))
 
     def close(self):
         for q, p in getattr(self, "peers", {}).items():

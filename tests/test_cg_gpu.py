@@ -116,9 +116,18 @@ def _pcg_rank_worker(rank, world, port, dims, exchange, q):
         gid = m.gid(torch, "cuda")
         fg = torch.from_numpy(np.random.default_rng(2).standard_normal(
             (nx * (lx - 1) + 1) * (ny * (lx - 1) + 1) * (nz * (lx - 1) + 1))).cuda()
-        x, hist = pcg.solve(fg[gid], iters=15)
+        f = fg[gid].contiguous()
+        x, hist = pcg.solve(f, iters=15)
         torch.cuda.synchronize()
-        q.put((rank, x.cpu().numpy(), hist.cpu().numpy()))
+        x, hist = x.cpu().numpy(), hist.cpu().numpy()
+        graph_ok = None
+        if exchange == "peer":  # the whole multi-rank solve as a CUDA graph, replayed twice
+            graph_ok = True
+            for _ in range(2):
+                xg, hg = pcg.solve(f, iters=15, graph=True)
+                torch.cuda.synchronize()
+                graph_ok &= bool(np.array_equal(hg.cpu().numpy(), hist) and np.array_equal(xg.cpu().numpy(), x))
+        q.put((rank, x, hist, graph_ok))
         dist.barrier()
         if op.peer is not None:
             op.peer.close()
@@ -133,7 +142,8 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
     peer memory (CUDA IPC; axhelm_gs_box_peer + axhelm_peer_allreduce).  The
     iterates match the single-domain solve to reassociation of the dots, and
     with the peer all-reduce every rank holds the same residual history bit
-    for bit."""
+    for bit; with peer memory the whole multi-rank solve also runs as a
+    captured CUDA graph (device-side sequence numbers), bit-identical."""
     import socket
 
     import torch.multiprocessing as mp
@@ -153,8 +163,9 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
         p.start()
     res = {}
     for _ in range(world):
-        r, x, h = q.get(timeout=300)
+        r, x, h, gok = q.get(timeout=300)
         res[r] = (x, h)
+        assert gok is None or gok, f"rank {r}: graph replay differs from the eager solve"
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
