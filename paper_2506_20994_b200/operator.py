@@ -6,9 +6,12 @@ element-local part; gather-scatter and the mesh are reference non-goals,
 SPEC.md:14).  Per apply on rank r of a z-slab partition:
 
   stream S0: ax on the slab's two boundary element layers
-             -> PARTIAL top plane -> NCCL send up / recv from below
-             -> FINISH bottom plane -> NCCL send down / recv from above
+             -> PARTIAL top plane -> send up / recv from below
+             -> FINISH bottom plane -> send down / recv from above
              -> WRITE top plane
+             (exchange="peer": the three plane kernels write the neighbours'
+             buffers and flags over NVLink themselves — dist.PeerExchange;
+             exchange="nccl": plane buffers over NCCL send / recv)
   stream S1: ax on the interior element layers + the local DSSUM of every
              other shared node                              (overlaps the exchange)
   S0 waits S1
