@@ -40,7 +40,8 @@ def test_diagonal_matches_unit_vector_applies(torch):
     assert o.normwise_rel(got, np.where(mask > 0, want, 0.0)) <= 1e-13
 
 
-@pytest.mark.parametrize("dims,mode", [((3, 2, 2, 4), "strict"), ((2, 2, 3, 5), "fast"), ((2, 2, 2, 8), "fast")])
+@pytest.mark.parametrize("dims,mode", [((3, 2, 2, 4), "strict"), ((2, 2, 3, 5), "fast"), ((2, 2, 2, 8), "fast"),
+                                       ((3, 3, 3, 2), "strict"), ((1, 2, 2, 16), "fast"), ((2, 1, 3, 11), "strict")])
 def test_pcg_iterates_match_oracle(torch, dims, mode):
     nx, ny, nz, lx = dims
     m, op, pcg = _setup(torch, nx, ny, nz, lx, mode)
@@ -54,7 +55,8 @@ def test_pcg_iterates_match_oracle(torch, dims, mode):
     arrays["ud"] = np.zeros(m.shape)
     xw, hw = o.pcg(arrays, gid, pcg.mask.cpu().numpy(), f, 25)
     h = hist.cpu().numpy()
-    assert np.max(np.abs(h - hw) / hw) <= 1e-8
+    live = hw > 1e-24 * hw[0]  # before the residual reaches rounding level (tiny meshes converge early)
+    assert np.max(np.abs(h - hw)[live] / hw[live]) <= 1e-8
     assert o.normwise_rel(x.cpu().numpy(), xw) <= 1e-9
 
 

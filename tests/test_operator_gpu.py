@@ -32,7 +32,7 @@ def _oracle_assembled(op, u_np, nx, ny, nz, lx):
     return o.dssum(o.ax(arrays), o.box_mesh_gid(nx, ny, nz, lx))
 
 
-@pytest.mark.parametrize("dims", [(3, 2, 7, 5), (2, 3, 5, 8), (2, 2, 4, 3), (1, 2, 3, 12)])
+@pytest.mark.parametrize("dims", [(3, 2, 7, 5), (2, 3, 5, 8), (2, 2, 4, 3), (1, 2, 3, 12), (4, 3, 5, 2), (1, 1, 3, 16)])
 @pytest.mark.parametrize("mode", ["strict", "fast"])
 def test_schedules_equal_sequential_and_oracle(torch, dims, mode):
     from paper_2506_20994_b200.mesh import BoxMesh
