@@ -516,6 +516,9 @@ def ours_arm(args):
             e2e["value"] = round(pts * ws / (t_max * 1e-3) / 1e9, 4)
             e2e["pageable"]["ms_per_step"] = round(tp_max, 3)
             e2e["pageable"]["value"] = round(pts * ws / (tp_max * 1e-3) / 1e9, 4)
+            tr_max = maxrank_ms(e2e["resident_operator"]["ms_per_step"])
+            e2e["resident_operator"]["ms_per_step"] = round(tr_max, 3)
+            e2e["resident_operator"]["value"] = round(pts * ws / (tr_max * 1e-3) / 1e9, 4)
             e2e["h2d_bytes_per_step"] *= ws
             e2e["d2h_bytes_per_step"] *= ws
             e2e["aggregation"] = f"{ws} ranks, max time over ranks"
@@ -615,12 +618,37 @@ def e2e_leg(args, torch, lib, arr, device):
         ptimes.append(time.perf_counter() - t0)
     tp = statistics.fmean(ptimes)
     del pg
+    # a solver's view: the operator (matrices, h1, G) resident on the device,
+    # only u in and w out per step (pinned host buffers, same ABI kernel)
+    hu = torch.empty(arr["ud"].shape, dtype=torch.float64, pin_memory=True)
+    hw = torch.empty_like(hu, pin_memory=True)
+    hu.copy_(arr["ud"])
+    # __dace_ax_helm with u, w in host memory and the rest device pointers:
+    # the library pipelines u chunks in / w chunks out around the kernel
+    rptrs = [hw.data_ptr(), hu.data_ptr()] + [arr[n].data_ptr() for n in ABI[2:]]
+
+    def rstep():
+        assert lib.axhelm_apply_sync(*rptrs, nel, lx, mode) == 0
+
+    rstep()
+    ok_r = bool(torch.equal(hw, arr["wd"].cpu()))
+    rtimes = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        rstep()
+        rtimes.append(time.perf_counter() - t0)
+    tr = statistics.fmean(rtimes)
+    del hu, hw
     return {"value": round(pts / t / 1e9, 4), "unit": "GDOF/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": nel * lx ** 3 * 8, "steps": len(times),
             "ms_per_step": round(t * 1e3, 3), "api": "__dace_ax_helm body (axhelm_apply_sync), pinned host buffers",
             "matches_device_result": ok,
             "pageable": {"value": round(pts / tp / 1e9, 4), "ms_per_step": round(tp * 1e3, 3), "ok": bool(ok_pg),
-                         "api": "same call, ordinary (pageable) host memory"}}
+                         "api": "same call, ordinary (pageable) host memory"},
+            "resident_operator": {"value": round(pts / tr / 1e9, 4), "ms_per_step": round(tr * 1e3, 3),
+                                  "ok": ok_r, "h2d_bytes_per_step": pts * 8, "d2h_bytes_per_step": pts * 8,
+                                  "api": "__dace_ax_helm body with only u, w in (pinned) host memory and the "
+                                         "operator resident in HBM: u chunks in, apply, w chunks out, pipelined"}}
 
 
 def cpu_leg(args, lib):
