@@ -1,0 +1,37 @@
+"""The bench.py JSON contract, checked on the committed bench line
+(profiles/r01_bench_s7.json) and on the argument defaults (CPU only)."""
+
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_recorded_bench_line_has_the_contract_keys():
+    d = json.loads((ROOT / "profiles" / "r01_bench_s7.json").read_text())
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "cpu_baseline",
+              "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["metric"].startswith("ax_helm") and d["unit"] == "GDOF/s" and d["higher_is_better"] is True
+    assert d["warmup"] >= 3 and d["gpu_launches"] >= d["steps"] > 0
+    assert "workload" in d["config"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    c = d["cpu_baseline"]
+    assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["matches_device_result"] is True
+    k = d["clocks"]
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(k)
+    assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(k["reasons"])
+
+
+def test_bench_defaults_are_the_headline_configuration():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    assert bench.LX == 8 and bench.NEL == 1 << 18 and bench.BYTES_PER_POINT == 72
+    assert bench.flops_model(8, 32768) == 1_912_602_624  # frozen (reference tests/test_oracle.py:245)
