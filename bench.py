@@ -327,6 +327,8 @@ def ours_arm(args):
         ndev = torch.cuda.device_count()
         torch.cuda.set_device(local % ndev)
         backend = os.environ.get("AXHELM_DIST_BACKEND", "nccl")
+        if backend == "nccl" and ws > ndev:
+            backend = "gloo"  # ranks sharing a GPU (test boxes): NCCL refuses duplicate devices
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
         else:

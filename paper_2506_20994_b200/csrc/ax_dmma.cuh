@@ -58,7 +58,18 @@ __device__ __forceinline__ int ut_idx(int l, int j, int i) {
 
 // DOT: also accumulate sum_p u_p w_p over the CTA's elements (in a fixed
 // order) into dot_partial[blockIdx.x] — the PCG's <p, A p> without a pass.
-template <bool DOT>
+//
+// XF (X.xrun = nx > 0, box-mesh layers): the CTA walks one contiguous
+// segment of elements instead of a grid stride, so consecutive elements of
+// an x-run pass through it in order, and it sums the x-face nodes they share
+// — the nodes that lie on no y or z element face (rows j, k in 1..lx-2),
+// i.e. exactly the local DSSUM's class-2 nodes (mesh_gs.cu) — in the
+// epilogue: the i = 7 column of element e-1 stays in a register of lane
+// q = 3, is shuffled to lane q = 0 of element e, and both copies receive
+// (0.0 + w[e-1]) + w[e], the DSSUM's ascending-copy sum, bit for bit.  The
+// faces at segment seams are summed by xfold_seams afterwards.  The DSSUM
+// pass then skips class 2, the half of its time that is sector-bound.
+template <bool DOT, bool XF = false>
 __global__ void __launch_bounds__(DmCfg::NT)
 ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, const AxExt X) {
   using C = DmCfg;
@@ -74,6 +85,14 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, co
   const int g = lane >> 2, q = lane & 3;
   const int64_t stride = gridDim.x;
   const L2Pol pol = make_l2pol(X.keep_w);
+  // element walk: grid stride, or (XF) one contiguous segment per CTA
+  int64_t e_begin = blockIdx.x, e_end = nel, e_step = stride;
+  if constexpr (XF) {
+    const int64_t seg = (nel + stride - 1) / stride;
+    e_begin = (int64_t)blockIdx.x * seg;
+    e_end = e_begin + seg < nel ? e_begin + seg : nel;
+    e_step = 1;
+  }
 
   if (tid == 0) {
     for (int d = 0; d < C::D; ++d) mbar_init(&bars[d], 1);
@@ -82,8 +101,8 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, co
   __syncthreads();
   if (tid == 0)
     for (int d = 0; d < C::D; ++d) {
-      const int64_t e = blockIdx.x + d * stride;
-      if (e < nel) issue_group<8>(A, nel, e, bufs + d * C::BUF, &bars[d], pol.in);
+      const int64_t e = e_begin + d * e_step;
+      if (e < e_end) issue_group<8>(A, nel, e, bufs + d * C::BUF, &bars[d], pol.in);
     }
 
   // matrix fragments, fixed for the whole CTA
@@ -105,8 +124,9 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, co
   }
 
   double dot_acc = 0.0;
+  double carry[4] = {0.0, 0.0, 0.0, 0.0};  // XF: deferred i = 7 values (lane q = 3)
   int64_t n = 0;
-  for (int64_t e = blockIdx.x; e < nel; e += stride, ++n) {
+  for (int64_t e = e_begin; e < e_end; e += e_step, ++n) {
     const int b = (int)(n % C::D);
     double* buf = bufs + b * C::BUF;
     mbar_wait(&bars[b], (uint32_t)((n / C::D) & 1));
@@ -214,15 +234,32 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, co
       const int k = warp * 4 + kt;
       const int o = k * 64 + g * 8 + 2 * q;
       const double2 z = lds2(ST + o);
-      const double w0 = w[kt][0] + z.x, w1 = w[kt][1] + z.y;
-      stg_w2(wout + o, w0, w1, pol);
+      double w0 = w[kt][0] + z.x;
+      const double w1 = w[kt][1] + z.y;
       if constexpr (DOT) dot_acc = fma(uown[kt][0], w0, fma(uown[kt][1], w1, dot_acc));
+      if constexpr (XF) {
+        const int64_t ex = e % X.xrun;
+        const bool row_in = k >= 1 && k <= 6 && g >= 1 && g <= 6;
+        const double prev = __shfl_sync(0xffffffffu, carry[kt], lane | 3);
+        if (q == 0 && row_in && ex > 0 && e > e_begin) {  // (k, g, 0) of e = (k, g, 7) of e-1
+          w0 = __dadd_rn(__dadd_rn(0.0, prev), w0);
+          stg_w(wout - C::L3 + o + 7, w0, pol);
+        }
+        if (q == 3 && row_in && ex < X.xrun - 1 && e + 1 < e_end) {  // deferred to element e+1
+          carry[kt] = w1;
+          stg_w(wout + o, w0, pol);
+        } else {
+          stg_w2(wout + o, w0, w1, pol);
+        }
+      } else {
+        stg_w2(wout + o, w0, w1, pol);
+      }
     }
     __syncthreads();  // buffer b and ST free
     if (tid == 0) {
       if (X.progress) signal_done(X, e, 1);
-      const int64_t en = e + C::D * stride;
-      if (en < nel) {
+      const int64_t en = e + C::D * e_step;
+      if (en < e_end) {
         fence_proxy_async();
         issue_group<8>(A, nel, en, buf, &bars[b], pol.in);
       }
@@ -240,6 +277,20 @@ ax_dmma8(const AxPtrs A, const int64_t nel, double* __restrict__ dot_partial, co
       dot_partial[blockIdx.x] = t;
     }
   }
+}
+
+// XF seams: the x-face shared by the last element of one CTA's segment and
+// the first of the next (same x-run), class-2 rows only; one CTA per seam.
+__global__ void __launch_bounds__(64) xfold_seams(double* __restrict__ w, const int64_t nel,
+                                                  const int64_t seg, const int xrun) {
+  const int64_t a = ((int64_t)blockIdx.x + 1) * seg;
+  if (a >= nel || a % xrun == 0) return;
+  const int k = threadIdx.x >> 3, j = threadIdx.x & 7;
+  if (k < 1 || k > 6 || j < 1 || j > 6) return;
+  double* p = w + a * DmCfg::L3 + k * 64 + j * 8;
+  const double s = __dadd_rn(__dadd_rn(0.0, p[7 - DmCfg::L3]), p[0]);
+  p[7 - DmCfg::L3] = s;
+  p[0] = s;
 }
 
 }  // namespace axb

@@ -60,6 +60,11 @@ struct AxExt {
   // loaded L2 evict-first and w is stored evict-normal so it stays in L2;
   // 0 (default): w is streamed out evict-first.
   int keep_w = 0;
+  // > 0 (DMMA kernel only): elements form x-runs of this length (box mesh,
+  // e = (ez ny + ey) nx + ex) and each CTA takes one contiguous element
+  // segment, summing the x-face nodes shared by consecutive elements of a
+  // run (the DSSUM's class-2 nodes) in its epilogue — see ax_dmma8
+  int xrun = 0;
   // optional completion counters for a concurrent consumer (the DSSUM
   // follower, mesh_gs.cu): after an element's w is stored, progress[e / lay]
   // is incremented with release semantics at gpu scope

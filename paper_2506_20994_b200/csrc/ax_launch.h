@@ -38,8 +38,10 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
 
 // structured DSSUM of the slab's node planes [zlo, zhi] (mesh_gs.cu);
 // gs_box_range_check returns nullptr or why the arguments are invalid
+// [s2lo, s2hi]: planes whose class-2 (x-face-only) nodes the x-folding DMMA
+// apply has summed already (skipped here)
 cudaError_t gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
-                         int64_t zhi, cudaStream_t st);
+                         int64_t zhi, cudaStream_t st, int64_t s2lo = 1, int64_t s2hi = 0);
 const char* gs_box_range_check(int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
                                int64_t zhi);
 

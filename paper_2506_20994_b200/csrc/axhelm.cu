@@ -210,6 +210,10 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
                                          (int)C::SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(ax_dmma8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ax_dmma8<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ax_dmma8<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     int b = 0;
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_dmma8<true>, C::NT, C::SMEM);
     if (e != cudaSuccess) {
@@ -222,12 +226,26 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
   return (int)(grid > nel ? nel : grid);
 }
 
+// X.xrun > 0: the x-folding variant (contiguous segments) + its seam pass
+template <bool DOT>
+static cudaError_t launch_dmma8_impl(const AxPtrs& A, int64_t nel, double* partial, int grid,
+                                     cudaStream_t st, const AxExt& X) {
+  if (X.xrun <= 0) {
+    ax_dmma8<DOT><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial, X);
+    return cudaGetLastError();
+  }
+  ax_dmma8<DOT, true><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial, X);
+  const int64_t seg = (nel + grid - 1) / grid;
+  const int64_t nseams = (nel - 1) / seg;  // segment starts a = c * seg < nel, c >= 1
+  if (nseams > 0) xfold_seams<<<(unsigned)nseams, 64, 0, st>>>(A.w, nel, seg, X.xrun);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_dmma8(const AxPtrs& A, int64_t nel, cudaStream_t st, const AxExt& X) {
   cudaError_t e;
   const int grid = dmma8_grid(nel, &e);
   if (e != cudaSuccess) return e;
-  ax_dmma8<false><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, nullptr, X);
-  return cudaGetLastError();
+  return launch_dmma8_impl<false>(A, nel, nullptr, grid, st, X);
 }
 
 bool progress_capable(const AxPtrs& A, int lx) {
@@ -244,9 +262,8 @@ cudaError_t launch_dmma8_dot(const AxPtrs& A, int64_t nel, double* partial, int*
   cudaError_t e;
   const int grid = dmma8_grid(nel, &e);
   if (e != cudaSuccess) return e;
-  ax_dmma8<true><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial, X);
   *nparts = grid;
-  return cudaGetLastError();
+  return launch_dmma8_impl<true>(A, nel, partial, grid, st, X);
 }
 
 static bool aligned16(const AxPtrs& A) {

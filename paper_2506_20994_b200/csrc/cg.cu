@@ -482,6 +482,14 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     schedule = AXHELM_SCHED_SEQUENTIAL;
   }
   const int64_t B = schedule > 0 ? schedule : (l1 - l0 > 0 ? l1 - l0 : 1);
+  // x-folding apply (ax_dmma.cuh, XF): the DMMA kernel sums the class-2
+  // (x-face-only) nodes of its layers itself; the DSSUM pass skips those
+  // planes' class 2.  Needs every class-2 plane of [l0, l1) in this call's
+  // range [zlo, zhi], and nothing else in the call reading unassembled w.
+  const int64_t s2lo = (ez0 + l0) * n1 + 1, s2hi = (ez0 + l1) * n1 - 1;
+  const char* xf_env = getenv("AXHELM_XFOLD");
+  const bool xfold = l1 > l0 && nx > 1 && n1 > 1 && !(xf_env && xf_env[0] == '0') && zlo <= s2lo &&
+                     zhi >= s2hi && dmma8_selected(ptrs_at(l0), lx, mode);
   int64_t next = zlo;  // first plane not yet summed
   int nchunks = 0;
   for (int64_t a = l0; a < l1 && e == cudaSuccess; a += B, ++nchunks) {
@@ -489,6 +497,7 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     AxPtrs A = ptrs_at(a);
     AxExt X;
     X.keep_w = schedule > 0 ? 1 : 0;
+    X.xrun = xfold ? nx : 0;
     const int64_t nel = (b - a) * lay;
     e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st, X)
                 : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
@@ -497,11 +506,14 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     // the layers above l1 are done by the caller
     const int64_t top = (b == l1) ? zhi : ((ez0 + b) * n1 - 1 < zhi ? (ez0 + b) * n1 - 1 : zhi);
     if (top >= next) {
-      e = gs_box_range(wd, nx, ny, lx, ez0, ez1, next, top, st);
+      e = xfold ? gs_box_range(wd, nx, ny, lx, ez0, ez1, next, top, st, s2lo, s2hi)
+                : gs_box_range(wd, nx, ny, lx, ez0, ez1, next, top, st);
       next = top + 1;
     }
   }
-  if (e == cudaSuccess && next <= zhi) e = gs_box_range(wd, nx, ny, lx, ez0, ez1, next, zhi, st);
+  if (e == cudaSuccess && next <= zhi)
+    e = xfold ? gs_box_range(wd, nx, ny, lx, ez0, ez1, next, zhi, st, s2lo, s2hi)
+              : gs_box_range(wd, nx, ny, lx, ez0, ez1, next, zhi, st);
   if (e == cudaSuccess && dot_out) {
     if (nchunks == 0) {
       e = cudaMemsetAsync(dot_out, 0, sizeof(double), st);

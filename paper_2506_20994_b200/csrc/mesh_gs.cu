@@ -441,8 +441,27 @@ __global__ void gs_box_local_kernel(double* __restrict__ w, const BoxGS M, int z
 // Local DSSUM of the owned node planes [lo, hi] (global z node-plane
 // indices; every copy of those nodes lies in the slab): three launches, one
 // per node class.
+// class-2 nodes of non-face planes [a, b]
 template <int LX>
-static void gs_box_local_range(double* w, const BoxGS& M, int lo, int hi, cudaStream_t st) {
+static void gs_box_cls2(double* w, const BoxGS& M, int a, int b, cudaStream_t st) {
+  constexpr int n1 = LX - 1;
+  if (n1 < 2 || M.nx < 2 || b < a) return;
+  const int fa = (a + n1 - 1) / n1, fb = b / n1;
+  const int nnf = (b - a + 1) - (fb >= fa ? fb - fa + 1 : 0);
+  if (nnf <= 0) return;
+  const int a2 = (a % n1 == 0) ? a + 1 : a;
+  const int qlo = (a2 / n1) * (n1 - 1) + (a2 % n1 - 1);
+  gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
+                                    (unsigned)((int64_t)M.ny * (n1 - 1) + GsNB<2>::NB - 1) / GsNB<2>::NB,
+                                    (unsigned)nnf),
+                               128, 0, st>>>(w, M, a, b, qlo, M.ny * (n1 - 1));
+}
+
+// [s2lo, s2hi]: node planes whose class-2 nodes are already summed (the
+// x-folding DMMA apply, ax_dmma.cuh); class 2 runs on [lo, hi] minus them
+template <int LX>
+static void gs_box_local_range(double* w, const BoxGS& M, int lo, int hi, cudaStream_t st,
+                               int s2lo = 1, int s2hi = 0) {
   constexpr int n1 = LX - 1;
   if (hi < lo) return;
   const dim3 blk(128);
@@ -462,10 +481,13 @@ static void gs_box_local_range(double* w, const BoxGS& M, int lo, int hi, cudaSt
       // y: non-face planes (batched), z: y-face rows
       gs_box_local_kernel<LX, 1><<<dim3(gxb, nb(nnf, GsNB<1>::NB), (unsigned)(M.ny + 1)), blk, 0,
                                    st>>>(w, M, lo, hi, qlo, nnf);
-      if (M.nx > 1)  // y: non-face rows, z: non-face planes
-        gs_box_local_kernel<LX, 2><<<dim3((unsigned)((M.nx - 1 + 127) / 128),
-                                          nb((int64_t)M.ny * (n1 - 1), GsNB<2>::NB), (unsigned)nnf),
-                                     blk, 0, st>>>(w, M, lo, hi, qlo, M.ny * (n1 - 1));
+      // y: non-face rows, z: non-face planes
+      if (s2hi < s2lo || s2hi < lo || s2lo > hi) {
+        gs_box_cls2<LX>(w, M, lo, hi, st);
+      } else {
+        gs_box_cls2<LX>(w, M, lo, s2lo - 1, st);
+        gs_box_cls2<LX>(w, M, s2hi + 1, hi, st);
+      }
     }
   }
 }
@@ -697,14 +719,14 @@ cudaError_t gs_box_follow(double* w, int nx, int ny, int lx, int64_t ez0, int64_
 namespace axb {
 // enqueue the local DSSUM of node planes [zlo, zhi] (validated by the caller)
 cudaError_t gs_box_range(double* w, int nx, int ny, int lx, int64_t ez0, int64_t ez1, int64_t zlo,
-                         int64_t zhi, cudaStream_t st) {
+                         int64_t zhi, cudaStream_t st, int64_t s2lo, int64_t s2hi) {
   const int n1 = lx - 1;
   BoxGS M{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1};
   if (zhi < zlo) return cudaSuccess;
   switch (lx) {
 #define AXB_GSR(N) \
   case N:          \
-    gs_box_local_range<N>(w, M, (int)zlo, (int)zhi, st); \
+    gs_box_local_range<N>(w, M, (int)zlo, (int)zhi, st, (int)s2lo, (int)s2hi); \
     break;
     AXB_GSR(2) AXB_GSR(3) AXB_GSR(4) AXB_GSR(5) AXB_GSR(6) AXB_GSR(7) AXB_GSR(8) AXB_GSR(9)
     AXB_GSR(10) AXB_GSR(11) AXB_GSR(12) AXB_GSR(13) AXB_GSR(14) AXB_GSR(15) AXB_GSR(16)

@@ -68,6 +68,38 @@ def test_schedules_equal_sequential_and_oracle(torch, dims, mode):
     assert abs(float(d0) - dw) <= 1e-11 * max(1.0, abs(dw))
 
 
+@pytest.mark.parametrize("dims", [(17, 9, 33), (64, 4, 16), (2, 1, 700), (5, 7, 3), (1, 6, 40)])
+@pytest.mark.parametrize("block", ["sequential", 3])
+def test_xfold_apply_bit_identical(torch, dims, block, monkeypatch):
+    """lx = 8 fast: the x-folding DMMA apply (class-2 DSSUM nodes summed in
+    its epilogue, segment seams by xfold_seams) gives w bit-identical to the
+    plain apply + full DSSUM pass (AXHELM_XFOLD=0), and matches the oracle.
+    Sizes chosen so CTA segments end mid x-run (seams), at run ends, and
+    with one element per CTA; nx = 1 has no x faces (xfold off)."""
+    from paper_2506_20994_b200.mesh import BoxMesh
+    from paper_2506_20994_b200.operator import HelmholtzOperator
+
+    nx, ny, nz = dims
+    lx = 8
+    m = BoxMesh(nx, ny, nz, lx)
+    op = HelmholtzOperator(m, torch, "cuda", mode="fast", schedule=block)
+    u_np = np.random.default_rng(nx * ny + nz).standard_normal(m.shape)
+    u = torch.from_numpy(u_np).cuda()
+    w = torch.full_like(u, np.nan)
+    d = torch.zeros(1, dtype=torch.float64, device="cuda")
+    op.apply(u, w, dot=d)
+    monkeypatch.setenv("AXHELM_XFOLD", "0")
+    w0 = torch.full_like(u, np.nan)
+    d0 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    op.apply(u, w0, dot=d0)
+    torch.cuda.synchronize()
+    assert torch.equal(w, w0)
+    assert abs(float(d) - float(d0)) <= 1e-12 * max(1.0, abs(float(d0)))
+    if m.nel <= 6000:
+        want = _oracle_assembled(op, u_np, nx, ny, nz, lx)
+        assert o.normwise_rel(w.cpu().numpy(), want) <= 1e-12
+
+
 def test_ax_gs_box_rejects_bad_ranges(torch):
     import ctypes
 
@@ -135,6 +167,8 @@ def _rank_worker(rank, world, port, dims, mode, block, q, exchange="nccl", appli
                                                             ("fast", (2, 3, 8, 8), "follow", "nccl", 2),
                                                             ("strict", (3, 2, 8, 5), "sequential", "peer", 2),
                                                             ("fast", (2, 3, 8, 8), "sequential", "peer", 2),
+                                                            ("fast", (5, 3, 12, 8), "sequential", "nccl", 2),
+                                                            ("fast", (4, 2, 12, 8), 2, "peer", 3),
                                                             ("strict", (2, 2, 9, 4), "sequential", "peer", 3)])
 def test_ranks_on_one_gpu_bit_exact(torch, mode, dims, block, exchange, world):
     """z-slab ranks with the overlapped boundary/interior apply and the
