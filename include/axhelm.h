@@ -232,16 +232,31 @@ int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const doub
                      const double* h1d, const double* g11d, const double* g22d, const double* g33d,
                      const double* g12d, const double* g13d, const double* g23d, int64_t nel,
                      int lx, int mode, double* partial, double* out, void* stream);
+/* axhelm_apply / axhelm_apply_dot (dot_out may be NULL) for nel elements that
+ * form whole x-runs of a brick (e = (ez ny + ey) nx + ex, nel % nx == 0).
+ * When the lx = 8 fast DMMA kernel runs, it also sums the class-2 DSSUM
+ * nodes — x-face nodes on no y / z element face, shared by consecutive
+ * elements of a run — in its epilogue, bit for bit as the DSSUM would
+ * ((0.0 + w[e-1]) + w[e]), and sets *xfolded = 1; else *xfolded = 0 and w
+ * is the plain element-local apply.  Pass *xfolded on to
+ * axhelm_cg_update_box.  AXHELM_XFOLD=0 in the environment disables it. */
+int axhelm_apply_box(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int nx, int64_t nel,
+                     int lx, int mode, double* partial, double* dot_out, int* xfolded, void* stream);
 /* Structured-brick PCG update with the local DSSUM folded in: w = A_local p
  * after the interface-plane exchange (axhelm_gs_box ops 1..3) but WITHOUT the
  * local DSSUM; each point gathers its node's local copies in the DSSUM's
  * order (bit-identical assembled value), r -= (a[0]/a[1]) QQ^T w, and
  * out = (sum cwt r dinv r, sum cwt r r) with cwt = mask/multiplicity computed
  * from the point's position (mask: the brick's outer boundary).  The slab is
- * element layers [ez0, ez1) of an nx*ny*nz brick. */
+ * element layers [ez0, ez1) of an nx*ny*nz brick.  xfolded: w came from
+ * axhelm_apply_box with *xfolded = 1 (class-2 nodes already summed: read
+ * once, not gathered). */
 int axhelm_cg_update_box(double* r, const double* w, const double* dinv, const double* a, int nx,
                          int ny, int64_t nz, int lx, int64_t ez0, int64_t ez1, int has_below,
-                         int has_above, double* partial, double* out, void* stream);
+                         int has_above, int xfolded, double* partial, double* out, void* stream);
 /* x += (a[0]/a[1]) p; p = dinv r + (sc_new[0]/a[0]) p  (a = (rz_old, p.Ap)) */
 int axhelm_cg_xpupdate(double* x, double* p, const double* r, const double* dinv, const double* a,
                        const double* sc_new, int64_t n, void* stream);

@@ -57,7 +57,9 @@ PROTOTYPES = {
     "axhelm_cg_pupdate": (ctypes.c_int, [_vp] * 5 + [ctypes.c_int64, _vp]),
     "axhelm_cg_update_box": (ctypes.c_int, [_vp] * 4 + [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
-                                                       _vp, _vp, _vp]),
+                                                       ctypes.c_int, _vp, _vp, _vp]),
+    "axhelm_apply_box": (ctypes.c_int, [_vp] * 15 + [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                     _vp, _vp, _vp, _vp]),
     "axhelm_cg_xpupdate": (ctypes.c_int, [_vp] * 6 + [ctypes.c_int64, _vp]),
     "axhelm_diag": (ctypes.c_int, [_vp] * 14 + [ctypes.c_int64, ctypes.c_int, _vp]),
     "axhelm_set_mode": (ctypes.c_int, [ctypes.c_int]),

@@ -157,7 +157,7 @@ class JacobiPCG:
                 self._check(self.lib.axhelm_cg_update_box(r.data_ptr(), w.data_ptr(), self.dinv.data_ptr(),
                                                           a[it].data_ptr(), m.nx, m.ny, m.nz, m.lx, m.ez0,
                                                           m.ez1, int(m.rank > 0), int(m.rank < m.world - 1),
-                                                          P, sc[it + 1].data_ptr(), s))
+                                                          int(self.op.xfolded), P, sc[it + 1].data_ptr(), s))
                 self._allreduce(sc[it + 1])
                 self._check(self.lib.axhelm_cg_xpupdate(x.data_ptr(), p.data_ptr(), r.data_ptr(),
                                                         self.dinv.data_ptr(), a[it].data_ptr(),

@@ -118,6 +118,7 @@ struct CgBox {
   BoxGS M;
   int64_t NZ;  // global node planes
   int has_below, has_above;
+  int xfolded;  // w's class-2 (x-face-only) nodes are already summed (x-folding apply)
 };
 
 // One element per block iteration (grid-stride over elements): the
@@ -166,10 +167,13 @@ __global__ void __launch_bounds__(RT, MINB) cg_update_box_kernel(double* __restr
       const bool loy = j == 0 && ey > 0, hiy = j == n1 && ey < M.ny - 1;
       const bool iface = (k == 0 && ezl == 0 && B.has_below) || (k == n1 && ezl == nl - 1 && B.has_above);
       const bool loz = !iface && k == 0 && ezl > 0, hiz = !iface && k == n1 && ezl < nl - 1;
-      const int cx = (lox || hix) && !iface ? 2 : 1, cy = (loy || hiy) && !iface ? 2 : 1;
+      // x copies to gather: none when the x-folding apply summed this node
+      // already (class 2: on an x face, on no y / z element face)
+      const bool xs = (lox || hix) && !iface && !(B.xfolded && j != 0 && j != n1 && k != 0 && k != n1);
+      const int cx = xs ? 2 : 1, cy = (loy || hiy) && !iface ? 2 : 1;
       const int cz = loz || hiz ? 2 : 1;
       single[u] = cx * cy * cz == 1;
-      const int64_t b0 = q - ((lox && !iface) ? DX : 0) - ((loy && !iface) ? DY : 0) - (loz ? DZ : 0);
+      const int64_t b0 = q - ((lox && xs) ? DX : 0) - ((loy && !iface) ? DY : 0) - (loz ? DZ : 0);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int dz = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
@@ -306,12 +310,12 @@ int axhelm_cg_update(double* x, double* r, const double* p, const double* w, con
 
 int axhelm_cg_update_box(double* r, const double* w, const double* dinv, const double* a, int nx,
                          int ny, int64_t nz, int lx, int64_t ez0, int64_t ez1, int has_below,
-                         int has_above, double* partial, double* out, void* stream) {
+                         int has_above, int xfolded, double* partial, double* out, void* stream) {
   if (lx < 2 || lx > 16 || nx < 1 || ny < 1 || ez0 < 0 || ez1 <= ez0 || ez1 > nz)
     return set_status(AXHELM_EINVAL, "axhelm_cg_update_box: bad sizes");
   const int n1 = lx - 1;
   CgBox B{BoxGS{nx, ny, lx, ez0, ez1, (int64_t)nx * n1 + 1, (int64_t)ny * n1 + 1}, nz * n1 + 1,
-          has_below, has_above};
+          has_below, has_above, xfolded ? 1 : 0};
   const int64_t nel = (ez1 - ez0) * nx * ny;
   if (nel >= ((int64_t)1 << 31)) return set_status(AXHELM_EINVAL, "axhelm_cg_update_box: too many elements");
   cudaStream_t st = (cudaStream_t)stream;
@@ -422,6 +426,32 @@ int axhelm_apply_dot(double* wd, const double* ud, const double* dxd, const doub
     return cuda_status(e, "axhelm_apply_dot");
   }
   return cuda_status(ax_dot(A, nel, lx, mode, partial, out, (cudaStream_t)stream, X), "axhelm_apply_dot");
+}
+
+int axhelm_apply_box(double* wd, const double* ud, const double* dxd, const double* dyd,
+                     const double* dzd, const double* dxtd, const double* dytd, const double* dztd,
+                     const double* h1d, const double* g11d, const double* g22d, const double* g33d,
+                     const double* g12d, const double* g13d, const double* g23d, int nx, int64_t nel,
+                     int lx, int mode, double* partial, double* dot_out, int* xfolded, void* stream) {
+  if (xfolded) *xfolded = 0;
+  if (lx < 2 || lx > 16 || nel < 0 || nx < 1 || nel % nx != 0)
+    return set_status(AXHELM_EINVAL, "axhelm_apply_box: bad sizes (nel must be whole x-runs of nx)");
+  if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
+    return set_status(AXHELM_EINVAL, "axhelm_apply_box: unknown mode %d", mode);
+  if (dot_out && !partial) return set_status(AXHELM_EINVAL, "axhelm_apply_box: dot needs partial scratch");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nel == 0) {
+    cudaError_t e = dot_out ? cudaMemsetAsync(dot_out, 0, sizeof(double), st) : cudaSuccess;
+    return cuda_status(e, "axhelm_apply_box");
+  }
+  AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+  AxExt X;
+  const char* xf_env = getenv("AXHELM_XFOLD");
+  if (nx > 1 && lx > 2 && !(xf_env && xf_env[0] == '0') && dmma8_selected(A, lx, mode)) X.xrun = nx;
+  cudaError_t e = dot_out ? ax_dot(A, nel, lx, mode, partial, dot_out, st, X)
+                          : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
+  if (e == cudaSuccess && xfolded) *xfolded = X.xrun > 0;
+  return cuda_status(e, "axhelm_apply_box");
 }
 
 int axhelm_ax_gs_scratch(int64_t nlayers) { return max_partials() + (int)(nlayers > 0 ? nlayers : 0); }

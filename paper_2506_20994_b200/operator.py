@@ -60,6 +60,13 @@ class HelmholtzOperator:
         self.dssum = SlabDSSUM(self.gs, comm, rank=mesh.rank, world=mesh.world)
         self.comm = comm
         self.overlap = overlap and mesh.world > 1 and (mesh.ez1 - mesh.ez0) > 2
+        # apply(local_dssum=False) through the x-folding kernel (class-2 DSSUM
+        # nodes summed by the apply; axhelm_apply_box).  Off by default: the
+        # PCG update's gathers of those copies hit L2 anyway, and the fold
+        # measured 2% slower per PCG iteration (3.40 -> 3.47 ms, same box);
+        # the assembled apply (local_dssum=True) always folds.
+        self.fold_unassembled = False
+        self.xfolded = False  # last apply(local_dssum=False): class-2 nodes summed by the apply
         self.side = torch.cuda.Stream(device) if self.overlap else None
         self.L3 = mesh.lx ** 3
         self._part = {}
@@ -88,10 +95,12 @@ class HelmholtzOperator:
 
     # ----------------------------------------------------------- pieces
 
-    def ax(self, u, w, e0: int = 0, e1: int | None = None, stream=None, dot=None):
+    def ax(self, u, w, e0: int = 0, e1: int | None = None, stream=None, dot=None, xfold: bool = False):
         """ax_helm on local elements [e0, e1) (stream-ordered).  dot: a device
         scalar receiving sum u*w over those elements (fused into the kernel
-        for lx = 8 fast mode)."""
+        for lx = 8 fast mode).  xfold: [e0, e1) are whole x-runs and the
+        x-folding apply may sum the class-2 DSSUM nodes (axhelm_apply_box);
+        returns whether it did."""
         m = self.mesh
         e1 = m.nel if e1 is None else e1
         n = e1 - e0
@@ -108,6 +117,15 @@ class HelmholtzOperator:
         if stream is None:
             stream = self.torch.cuda.current_stream(self.device)
         sp = ctypes.c_void_p(stream.cuda_stream)
+        if xfold:
+            flag = ctypes.c_int(0)
+            part = self._partials(stream) if dot is not None else None
+            rc = self.lib.axhelm_apply_box(*ptrs, m.nx, n, m.lx, self.mode,
+                                           part.data_ptr() if part is not None else None,
+                                           dot.data_ptr() if dot is not None else None, ctypes.byref(flag), sp)
+            if rc:
+                raise DeviceError(_lib.last_error(self.lib))
+            return bool(flag.value)
         if dot is None:
             rc = self.lib.axhelm_apply(*ptrs, n, m.lx, self.mode, sp)
         else:
@@ -150,7 +168,8 @@ class HelmholtzOperator:
         before assembly (= <u, QQ^T A u> for continuous u; PCG's p.Ap).
         local_dssum=False leaves the local shared nodes unassembled (only the
         interface planes are summed) for a consumer that gathers them itself
-        (axhelm_cg_update_box)."""
+        (axhelm_cg_update_box); self.xfolded then says whether the class-2
+        nodes came out summed already (x-folding apply)."""
         m = self.mesh
         torch = self.torch
         nl = m.ez1 - m.ez0
@@ -158,15 +177,16 @@ class HelmholtzOperator:
             if local_dssum:
                 self.ax_gs(u, w, 0, nl, dot=dot)
             else:
-                self.ax(u, w, dot=dot)
+                self.xfolded = bool(self.ax(u, w, dot=dot, xfold=self.fold_unassembled))
             self._exchange(w)
             return w
         s0 = torch.cuda.current_stream(self.device)
         lay = m.nx * m.ny
         d3 = self._dots if dot is not None else None
         # boundary element layers first (their results feed the exchange)
-        self.ax(u, w, 0, lay, dot=d3[0:1] if d3 is not None else None)
-        self.ax(u, w, m.nel - lay, m.nel, dot=d3[1:2] if d3 is not None else None)
+        xf = not local_dssum and self.fold_unassembled
+        f0 = self.ax(u, w, 0, lay, dot=d3[0:1] if d3 is not None else None, xfold=xf)
+        f1 = self.ax(u, w, m.nel - lay, m.nel, dot=d3[1:2] if d3 is not None else None, xfold=xf)
         self.side.wait_stream(s0)
         with torch.cuda.stream(self.side):
             # interior layers + every local DSSUM plane
@@ -174,7 +194,10 @@ class HelmholtzOperator:
             if local_dssum:
                 self.ax_gs(u, w, 1, nl - 1, stream=self.side, dot=dd)
             else:
-                self.ax(u, w, lay, m.nel - lay, stream=self.side, dot=dd)
+                f2 = self.ax(u, w, lay, m.nel - lay, stream=self.side, dot=dd, xfold=xf)
+                if not (bool(f0) == bool(f1) == bool(f2)):
+                    raise DeviceError("x-folding chosen for some element ranges only")
+                self.xfolded = bool(f0)
         self._exchange(w)
         s0.wait_stream(self.side)
         if dot is not None:

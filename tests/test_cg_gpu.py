@@ -96,7 +96,43 @@ def test_fused_update_matches_separate_passes(torch, dims, mode):
     assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-10
 
 
-def _pcg_rank_worker(rank, world, port, dims, exchange, q):
+@pytest.mark.parametrize("dims", [(17, 5, 9), (3, 2, 4), (1, 3, 5)])
+def test_xfold_update_bit_identical(torch, dims, monkeypatch):
+    """lx = 8 fast: apply(local_dssum=False) with the x-folding kernel (class-2
+    nodes summed by the apply, read once by the update) + axhelm_cg_update_box
+    gives r and the two update sums bit-identical to the plain apply whose
+    x copies the update gathers (AXHELM_XFOLD=0); nx = 1 never folds."""
+    import ctypes
+
+    nx, ny, nz = dims
+    m, op, pcg = _setup(torch, nx, ny, nz, 8, "fast")
+    op.fold_unassembled = True
+    g = torch.Generator(device="cuda").manual_seed(11)
+    p = torch.randn(m.shape, dtype=torch.float64, device="cuda", generator=g)
+    r0 = torch.randn(m.shape, dtype=torch.float64, device="cuda", generator=g)
+    a = torch.tensor([0.7, 1.3], dtype=torch.float64, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    res = []
+    for env in (None, "0"):
+        if env is not None:
+            monkeypatch.setenv("AXHELM_XFOLD", env)
+        w = torch.full_like(p, np.nan)
+        dot = torch.zeros(1, dtype=torch.float64, device="cuda")
+        op.apply(p, w, dot=dot, local_dssum=False)
+        r = r0.clone()
+        out = torch.zeros(2, dtype=torch.float64, device="cuda")
+        assert pcg.lib.axhelm_cg_update_box(r.data_ptr(), w.data_ptr(), pcg.dinv.data_ptr(), a.data_ptr(),
+                                            nx, ny, nz, 8, 0, nz, 0, 0, int(op.xfolded),
+                                            pcg.partial.data_ptr(), out.data_ptr(), s) == 0
+        torch.cuda.synchronize()
+        res.append((op.xfolded, r, out, float(dot)))
+    assert res[0][0] == (nx > 1) and res[1][0] is False
+    assert torch.equal(res[0][1], res[1][1])
+    assert torch.equal(res[0][2], res[1][2])
+    assert abs(res[0][3] - res[1][3]) <= 1e-12 * max(1.0, abs(res[1][3]))
+
+
+def _pcg_rank_worker(rank, world, port, dims, exchange, q, mode="strict"):
     import os
 
     import torch
@@ -113,7 +149,8 @@ def _pcg_rank_worker(rank, world, port, dims, exchange, q):
 
         nx, ny, nz, lx = dims
         m = BoxMesh(nx, ny, nz, lx, rank, world)
-        op = HelmholtzOperator(m, torch, "cuda", comm=TorchComm(dist), mode="strict", exchange=exchange)
+        op = HelmholtzOperator(m, torch, "cuda", comm=TorchComm(dist), mode=mode, exchange=exchange)
+        op.fold_unassembled = mode == "fast"
         pcg = JacobiPCG(op)
         gid = m.gid(torch, "cuda")
         fg = torch.from_numpy(np.random.default_rng(2).standard_normal(
@@ -137,8 +174,12 @@ def _pcg_rank_worker(rank, world, port, dims, exchange, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange,world", [("nccl", 2), ("peer", 2), ("peer", 3)])
-def test_pcg_ranks_on_one_gpu(torch, exchange, world):
+@pytest.mark.parametrize("exchange,world,mode,dims", [("nccl", 2, "strict", (2, 3, 9, 4)),
+                                                      ("peer", 2, "strict", (2, 3, 9, 4)),
+                                                      ("peer", 3, "strict", (2, 3, 9, 4)),
+                                                      ("nccl", 2, "fast", (3, 2, 9, 8)),
+                                                      ("peer", 2, "fast", (3, 2, 9, 8))])
+def test_pcg_ranks_on_one_gpu(torch, exchange, world, mode, dims):
     """Multi-rank PCG (z-slabs, ranks sharing one GPU): the interface exchange
     and the dot all-reduces through gloo ("nccl" transport path) or through
     peer memory (CUDA IPC; axhelm_gs_box_peer + axhelm_peer_allreduce).  The
@@ -152,7 +193,6 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
 
     from paper_2506_20994_b200.mesh import BoxMesh
 
-    dims = (2, 3, 9, 4)
     nx, ny, nz, lx = dims
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -160,7 +200,7 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_pcg_rank_worker, args=(r, world, port, dims, exchange, q)) for r in range(world)]
+    procs = [ctx.Process(target=_pcg_rank_worker, args=(r, world, port, dims, exchange, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -171,7 +211,7 @@ def test_pcg_ranks_on_one_gpu(torch, exchange, world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    m, op, pcg = _setup(torch, nx, ny, nz, lx, "strict")
+    m, op, pcg = _setup(torch, nx, ny, nz, lx, mode)
     gid = m.gid(torch, "cuda")
     fg = torch.from_numpy(np.random.default_rng(2).standard_normal(
         (nx * (lx - 1) + 1) * (ny * (lx - 1) + 1) * (nz * (lx - 1) + 1))).cuda()
