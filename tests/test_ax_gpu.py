@@ -321,3 +321,32 @@ def test_pageable_host_path_large_bit_exact(torch, kern):
     host["wd"][:] = np.nan
     kern["strict"](host, nel, lx)
     assert np.array_equal(host["wd"], want)
+
+
+@pytest.mark.parametrize("lx,nel", [(8, 37), (5, 41), (10, 9), (7, 12), (2, 101)])
+def test_misaligned_device_buffers(torch, kern, lx, nel):
+    """Field buffers 8 B off a 16-B boundary (views into a larger allocation,
+    as a caller slicing its own arena would pass): the 16-B TMA / DMMA paths
+    must detect it and fall back without changing a bit — strict equals the
+    oracle's bytes, fast stays within 1e-12."""
+    arrays = o.problem(lx, nel, seed=17 * lx + nel)
+    want = o.ax(arrays)
+    for mode in ("strict", "fast"):
+        dev = {}
+        for k, v in arrays.items():
+            if v.ndim == 4:
+                flat = torch.empty(v.size + 1, dtype=torch.float64, device="cuda")
+                view = flat[1:].view(v.shape)
+                assert view.data_ptr() % 16 == 8
+                view.copy_(torch.from_numpy(np.ascontiguousarray(v)))
+                dev[k] = view
+            else:
+                dev[k] = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        dev["wd"].fill_(np.nan)
+        kern[mode](dev, nel, lx)
+        torch.cuda.synchronize()
+        got = dev["wd"].cpu().numpy()
+        if mode == "strict":
+            assert o.digest(got) == o.digest(want)
+        else:
+            assert o.normwise_rel(got, want) <= FAST_TOL

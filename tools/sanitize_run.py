@@ -33,5 +33,15 @@ for sched in ("sequential", "follow", 1):
     op.apply(u, w, dot=d)
 pcg = JacobiPCG(op)
 pcg.solve(u * pcg.mask, iters=3)
+# x-folding apply with multi-element CTA segments (folds inside segments and
+# at seams), assembled and unassembled (PCG update reading folded nodes once)
+m = BoxMesh(16, 8, 8, 8)
+op = HelmholtzOperator(m, torch, "cuda", mode="fast")
+u = torch.randn(m.shape, dtype=torch.float64, device="cuda")
+w = torch.empty_like(u)
+op.apply(u, w)
+op.fold_unassembled = True
+pcg = JacobiPCG(op)
+pcg.solve(u * pcg.mask, iters=2)
 torch.cuda.synchronize()
 print("sanitize workload done")
