@@ -51,6 +51,8 @@ template <int LX>
 struct T2Shape {
   static constexpr int EPL = LX == 2 ? 32 : LX == 3 ? 14 : LX == 4 ? 8 : LX == 5 ? 5
                            : LX == 6 ? 3 : LX == 7 ? 2 : 1;
+  // (k-split at lx 5..7 too, with no register hint: 1.03-1.17x slower there,
+  // same-box A/B at the end of round 1)
   static constexpr int NKS = LX == 8 ? 2 : 1;
   static constexpr int D = LX >= 9 ? 1 : 2;
   // split issue of the next group (issue_group2_part), per mode from same-box
