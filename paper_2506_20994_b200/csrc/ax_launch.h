@@ -13,13 +13,12 @@ int set_status(int st, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 int default_mode();
 
-// enqueue one apply over device pointers (no validation).  hz / hzt / hx /
-// hxt: host copies of dzd / dztd / dxd / dxtd when the caller has them
-// (else looked up in / added to the pointer-keyed cache).
+// enqueue one apply over device pointers (no validation).  hz / hzt: host
+// copies of dzd / dztd when the caller has them (else looked up in / added
+// to the pointer-keyed cache without blocking).
 // X: keep-w-in-L2 / progress extensions (honoured by the lx = 8 DMMA kernel)
 cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
                       const double* hz = nullptr, const double* hzt = nullptr,
-                      const double* hx = nullptr, const double* hxt = nullptr,
                       const AxExt& X = AxExt{});
 
 // fused lx = 8 fast apply + per-CTA partials of sum u*w (nparts written)

@@ -303,7 +303,7 @@ template <int LX, bool FAST, int NKS, int DR = 2>
 __global__ void __launch_bounds__(T2Cfg<LX, NKS, DR>::NT, T2Cfg<LX, NKS, DR>::MINB)
 ax_tma2(const __grid_constant__ TParams<LX> P) {
   using C = T2Cfg<LX, NKS, DR>;
-  constexpr int L2 = C::L2, L3 = C::L3, FIELD = C::FIELD;
+  constexpr int L2 = C::L2, L3 = C::L3;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* bufs = reinterpret_cast<double*>(smem_raw + 128);

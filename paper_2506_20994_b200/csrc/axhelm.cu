@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -45,18 +46,39 @@ int cuda_status(cudaError_t e, const char* where) {
   return set_status(AXHELM_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------- per-device state
+//
+// Launch caches (max-dynamic-smem attribute done, resident CTAs per SM, SM
+// count) are per device: cudaFuncSetAttribute applies to the current
+// device's context only, so a process driving several GPUs needs one entry
+// per device.  Entries are written once (idempotent, benign race).
+constexpr int kMaxDev = 64;
+static int cur_dev() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return -1;
+  return d;
+}
+struct DevCache {
+  std::atomic<int> v[kMaxDev];
+  DevCache() {
+    for (auto& x : v) x.store(0, std::memory_order_relaxed);
+  }
+};
+
 // ---------------------------------------------------------------- launch
 
 template <int LX, bool FAST>
 static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
   using C = KCfg<LX>;
-  static bool attr_done = false;  // benign race: idempotent attribute set
-  if (!attr_done) {
+  static DevCache attr_done;
+  const int dev = cur_dev();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  if (!attr_done.v[dev].load(std::memory_order_relaxed)) {
     cudaError_t e = cudaFuncSetAttribute(ax_kwalk<LX, FAST>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done.v[dev].store(1, std::memory_order_relaxed);
   }
   const int64_t blocks = (nel + C::EPB - 1) / C::EPB;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -84,7 +106,7 @@ static int g_pf = [] {
   int d = v ? atoi(v) : 1;
   return (d >= 1 && d <= 3) ? d : 1;
 }();
-static int g_num_sms = 0;
+static DevCache g_num_sms;
 static bool aligned16(const AxPtrs& A);
 // AXHELM_CTAS_PER_SM caps the persistent kernels' resident CTAs per SM
 // (tuning knob; 0 = occupancy limit)
@@ -95,12 +117,15 @@ static int g_cta_cap = [] {
 static int cap_ctas(int b) { return (g_cta_cap > 0 && g_cta_cap < b) ? g_cta_cap : b; }
 
 static int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int dev = cur_dev();
+  if (dev < 0) return 1;
+  int n = g_num_sms.v[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 1;
+    g_num_sms.v[dev].store(n, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return n;
 }
 
 
@@ -108,57 +133,119 @@ static int num_sms() {
 //
 // The kernel verifies the copy against the device arrays and falls back to
 // them (flagging *stale) if they differ, so a stale cache costs speed, never
-// correctness.
+// correctness.  The cache never blocks the caller: a miss enqueues an async
+// D2H copy into the entry's pinned slot on the caller's stream (skipped while
+// the stream is being captured into a CUDA graph) and that launch runs the
+// kernel's shared-memory path; later launches use the copy once its event
+// has completed.  axhelm_apply therefore stays purely stream-ordered.
 struct MatEntry {
   const double* dz = nullptr;
   const double* dzt = nullptr;
   int lx = 0;
+  int dev = -1;
+  bool ready = false;
   uint64_t used = 0;
-  double z[256], zt[256];
+  double* h = nullptr;  // pinned: z at [0, 256), zt at [256, 512)
+  cudaEvent_t ev = nullptr;
 };
 static std::mutex g_mat_mu;
 static MatEntry g_mat[16];
 static uint64_t g_mat_clock = 0;
 static int* g_stale = nullptr;  // mapped pinned host flag
 
+// *have = true: z / zt hold the matrices (parameter path); false: the
+// caller poisons the parameter copy and passes no stale flag, so the kernel
+// reads the device arrays (the verification fails unless the bits match,
+// in which case the copy is exact anyway).
 static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, const double* hzt,
-                                 cudaStream_t st, double* z, double* zt, int** stale) {
+                                 cudaStream_t st, double* z, double* zt, int** stale, bool* have) {
   const size_t n = (size_t)lx * lx;
   std::lock_guard<std::mutex> lock(g_mat_mu);
+  *have = false;
+  *stale = nullptr;
   if (!g_stale) {
     cudaError_t e = cudaHostAlloc(&g_stale, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable);
     if (e != cudaSuccess) return e;
     *g_stale = 0;
   }
-  *stale = g_stale;
-  if (hz && hzt) {
+  if (hz && hzt) {  // caller's host copies (host-staged __dace_ax_helm)
     memcpy(z, hz, n * sizeof(double));
     memcpy(zt, hzt, n * sizeof(double));
+    *stale = g_stale;
+    *have = true;
     return cudaSuccess;
   }
   if (*(volatile int*)g_stale) {  // a kernel saw a changed matrix: drop every copy
-    for (auto& m : g_mat) m.dz = m.dzt = nullptr;
+    for (auto& m : g_mat) m.dz = m.dzt = nullptr, m.ready = false;
     *(volatile int*)g_stale = 0;
   }
+  const int dev = cur_dev();
   MatEntry* hit = nullptr;
   MatEntry* lru = &g_mat[0];
   for (auto& m : g_mat) {
-    if (m.dz == A.dz && m.dzt == A.dzt && m.lx == lx) hit = &m;
+    if (m.dz == A.dz && m.dzt == A.dzt && m.lx == lx && m.dev == dev) hit = &m;
     if (m.used < lru->used) lru = &m;
   }
-  if (!hit) {
-    hit = lru;
-    cudaError_t e = cudaMemcpyAsync(hit->z, A.dz, n * sizeof(double), cudaMemcpyDefault, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hit->zt, A.dzt, n * sizeof(double), cudaMemcpyDefault, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return e;
-    hit->dz = A.dz;
-    hit->dzt = A.dzt;
-    hit->lx = lx;
+  if (hit && !hit->ready) {  // fetch in flight: ready once its event has completed
+    const cudaError_t q = cudaEventQuery(hit->ev);
+    if (q == cudaSuccess) hit->ready = true;
+    else if (q == cudaErrorNotReady) (void)cudaGetLastError();
+    else return q;
   }
-  hit->used = ++g_mat_clock;
-  memcpy(z, hit->z, n * sizeof(double));
-  memcpy(zt, hit->zt, n * sizeof(double));
+  if (hit && hit->ready) {
+    hit->used = ++g_mat_clock;
+    memcpy(z, hit->h, n * sizeof(double));
+    memcpy(zt, hit->h + 256, n * sizeof(double));
+    *stale = g_stale;
+    *have = true;
+    return cudaSuccess;
+  }
+  if (hit) return cudaSuccess;  // still in flight
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusNone) return cudaSuccess;  // no side effects inside a capture
+  MatEntry& m = *lru;
+  if (!m.h && (e = cudaHostAlloc(&m.h, 512 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess) return e;
+  if (m.ev && m.dev != dev) {
+    cudaEventDestroy(m.ev);  // events belong to the device they were created on
+    m.ev = nullptr;
+  }
+  if (!m.ev && (e = cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  m.dz = m.dzt = nullptr;
+  m.ready = false;
+  if ((e = cudaMemcpyAsync(m.h, A.dz, n * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(m.h + 256, A.dzt, n * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaEventRecord(m.ev, st)) != cudaSuccess)
+    return e;
+  m.dz = A.dz;
+  m.dzt = A.dzt;
+  m.lx = lx;
+  m.dev = dev;
+  m.used = ++g_mat_clock;
+  return cudaSuccess;
+}
+
+// fill the kernel's transposed parameter copies (zT[k][l] = dz[l][k]) or
+// poison them (shared-memory path, see host_matrices)
+template <int LX>
+static cudaError_t param_matrices(TParams<LX>& P, cudaStream_t st, const double* hz, const double* hzt) {
+  double z[LX * LX], zt[LX * LX];
+  bool have = false;
+  cudaError_t e = host_matrices(P.A, LX, hz, hzt, st, z, zt, &P.stale, &have);
+  if (e != cudaSuccess) return e;
+  if (!have) {
+    const long long bits = 0x7ff4deadbeef0001LL;
+    double poison;
+    memcpy(&poison, &bits, sizeof poison);
+    for (int q = 0; q < LX * LX; ++q) P.zT[q] = P.ztT[q] = poison;
+    return cudaSuccess;
+  }
+  for (int l = 0; l < LX; ++l)
+    for (int k = 0; k < LX; ++k) {
+      P.zT[k * LX + l] = z[l * LX + k];
+      P.ztT[k * LX + l] = zt[l * LX + k];
+    }
   return cudaSuccess;
 }
 
@@ -168,31 +255,37 @@ static int g_nks8 = [] {
   return (d >= 1 && d <= 4) ? d : 2;
 }();
 
+// resident CTAs per SM of `kern` at `smem` bytes, per device; sets the
+// max-dynamic-shared-memory attribute on first use on each device
+template <typename K>
+static cudaError_t ctas_per_sm(DevCache& cache, K kern, int nt, size_t smem, int* out) {
+  const int dev = cur_dev();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  int b = cache.v[dev].load(std::memory_order_relaxed);
+  if (b == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, nt, smem);
+    if (e != cudaSuccess) return e;
+    b = cap_ctas(b > 0 ? b : 1);
+    cache.v[dev].store(b, std::memory_order_relaxed);
+  }
+  *out = b;
+  return cudaSuccess;
+}
+
 template <int LX, bool FAST, int NKS, int D = 2>
 static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
                                const double* hzt) {
   using C = T2Cfg<LX, NKS, D>;
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_tma2<LX, FAST, NKS, D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_tma2<LX, FAST, NKS, D>, C::NT, C::SMEM);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm = cap_ctas(b > 0 ? b : 1);
-  }
+  static DevCache occ;
+  int blocks_per_sm = 0;
+  cudaError_t e = ctas_per_sm(occ, ax_tma2<LX, FAST, NKS, D>, C::NT, C::SMEM, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
   TParams<LX> P;
   P.A = A;
   P.nel = nel;
-  double z[LX * LX], zt[LX * LX];
-  cudaError_t e = host_matrices(A, LX, hz, hzt, st, z, zt, &P.stale);
-  if (e != cudaSuccess) return e;
-  for (int l = 0; l < LX; ++l)
-    for (int k = 0; k < LX; ++k) {
-      P.zT[k * LX + l] = z[l * LX + k];
-      P.ztT[k * LX + l] = zt[l * LX + k];
-    }
+  if ((e = param_matrices<LX>(P, st, hz, hzt)) != cudaSuccess) return e;
   const int64_t groups = (nel + C::EPL - 1) / C::EPL;
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   if (grid > groups) grid = groups;
@@ -200,11 +293,16 @@ static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, co
   return cudaGetLastError();
 }
 
-
 static int dmma8_grid(int64_t nel, cudaError_t* err) {
   using C = DmCfg;
-  static int blocks_per_sm = 0;
+  static DevCache occ;
   *err = cudaSuccess;
+  const int dev = cur_dev();
+  if (dev < 0) {
+    *err = cudaErrorInvalidDevice;
+    return 0;
+  }
+  int blocks_per_sm = occ.v[dev].load(std::memory_order_relaxed);
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(ax_dmma8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
@@ -221,6 +319,7 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
       return 0;
     }
     blocks_per_sm = cap_ctas(b > 0 ? b : 1);
+    occ.v[dev].store(blocks_per_sm, std::memory_order_relaxed);
   }
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   return (int)(grid > nel ? nel : grid);
@@ -230,6 +329,9 @@ static int dmma8_grid(int64_t nel, cudaError_t* err) {
 template <bool DOT>
 static cudaError_t launch_dmma8_impl(const AxPtrs& A, int64_t nel, double* partial, int grid,
                                      cudaStream_t st, const AxExt& X) {
+  // the x-folding epilogue writes element e's shared x-face after e + 1 is
+  // done, so per-element progress counters would announce unassembled w
+  if (X.xrun > 0 && X.progress) return cudaErrorInvalidValue;
   if (X.xrun <= 0) {
     ax_dmma8<DOT><<<grid, DmCfg::NT, DmCfg::SMEM, st>>>(A, nel, partial, X);
     return cudaGetLastError();
@@ -276,18 +378,10 @@ static bool aligned16(const AxPtrs& A) {
 template <int LX, bool FAST, int PF>
 static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
   using C = SCfg<LX>;
-  static int blocks_per_sm = 0;  // benign race: idempotent
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_kwalk_pf<LX, FAST, PF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ax_kwalk_pf<LX, FAST, PF>, C::NT,
-                                                      C::SMEM);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm = b > 0 ? b : 1;
-  }
+  static DevCache occ;
+  int blocks_per_sm = 0;
+  cudaError_t e = ctas_per_sm(occ, ax_kwalk_pf<LX, FAST, PF>, C::NT, C::SMEM, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
   const int64_t groups = (nel + C::EPB - 1) / C::EPB;
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   if (grid > groups) grid = groups;
@@ -297,8 +391,7 @@ static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 
 template <int LX, bool FAST>
 static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
-                                  const double* hzt, const double* hx, const double* hxt,
-                                  const AxExt& X) {
+                                  const double* hzt, const AxExt& X) {
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
   if constexpr (LX <= 8) {
     if ((g_variant == 6 || g_variant == 0) && FAST && aligned16(A)) {
@@ -326,20 +419,18 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
 
 template <int LX>
 static cudaError_t launch_lx(const AxPtrs& A, int64_t nel, int mode, cudaStream_t st,
-                             const double* hz, const double* hzt, const double* hx,
-                             const double* hxt, const AxExt& X) {
-  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, hx, hxt, X)
-                             : launch_variant<LX, false>(A, nel, st, hz, hzt, hx, hxt, X);
+                             const double* hz, const double* hzt, const AxExt& X) {
+  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, X)
+                             : launch_variant<LX, false>(A, nel, st, hz, hzt, X);
 }
 
 cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
-                      const double* hz, const double* hzt, const double* hx, const double* hxt,
-                      const AxExt& X) {
+                      const double* hz, const double* hzt, const AxExt& X) {
   if (nel == 0) return cudaSuccess;
   switch (lx) {
 #define AXB_CASE(N) \
   case N:           \
-    return launch_lx<N>(A, nel, mode, st, hz, hzt, hx, hxt, X);
+    return launch_lx<N>(A, nel, mode, st, hz, hzt, X);
     AXB_CASE(2) AXB_CASE(3) AXB_CASE(4) AXB_CASE(5) AXB_CASE(6) AXB_CASE(7)
     AXB_CASE(8) AXB_CASE(9) AXB_CASE(10) AXB_CASE(11) AXB_CASE(12)
     AXB_CASE(13) AXB_CASE(14) AXB_CASE(15) AXB_CASE(16)
@@ -349,12 +440,14 @@ cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream
   }
 }
 
-static int g_mode = [] {
+// __dace_ax_helm's mode: process-wide, set from any thread (atomic)
+static std::atomic<int> g_mode{[] {
   const char* v = getenv("AXHELM_FP");
-  return (v && (!strcmp(v, "fast") || !strcmp(v, "FAST"))) ? AXHELM_FAST : AXHELM_STRICT;
-}();
+  return (v && (!strcmp(v, "fast") || !strcmp(v, "FAST"))) ? (int)AXHELM_FAST : (int)AXHELM_STRICT;
+}()};
 
-int default_mode() { return g_mode; }
+int default_mode() { return g_mode.load(std::memory_order_relaxed); }
+
 
 }  // namespace axb
 
@@ -384,7 +477,7 @@ int axhelm_apply(double* wd, const double* ud, const double* dxd, const double* 
   AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   AxExt X;
   X.keep_w = keep;
-  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr, X),
+  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream, nullptr, nullptr, X),
                      "axhelm_apply");
 }
 
@@ -398,7 +491,7 @@ void __dace_ax_helm(double* AXH_RESTRICT wd, const double* AXH_RESTRICT ud,
                     const double* AXH_RESTRICT g23d, int nelv, int lx) {
   const double* ptrs[15] = {wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd,
                             h1d, g11d, g22d, g33d, g12d, g13d, g23d};
-  host_or_device_apply(ptrs, (int64_t)nelv, lx, g_mode);
+  host_or_device_apply(ptrs, (int64_t)nelv, lx, default_mode());
 }
 
 int axhelm_apply_sync(double* wd, const double* ud, const double* dxd, const double* dyd,
@@ -417,11 +510,11 @@ int axhelm_apply_sync(double* wd, const double* ud, const double* dxd, const dou
 int axhelm_set_mode(int mode) {
   if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
     return set_status(AXHELM_EINVAL, "unknown mode %d", mode);
-  g_mode = mode;
+  g_mode.store(mode, std::memory_order_relaxed);
   return set_status(AXHELM_OK, "");
 }
 
-int axhelm_get_mode(void) { return g_mode; }
+int axhelm_get_mode(void) { return default_mode(); }
 int axhelm_last_status(void) { return t_status; }
 const char* axhelm_last_error(void) { return t_msg; }
 const char* axhelm_version(void) { return "libaxhelm_sm100 " AXHELM_VERSION " (sm_100a, FP64)"; }
@@ -431,14 +524,10 @@ int axhelm_probe_stream(double* wd, const double* ud, const double* h1d, const d
                         const double* g13d, const double* g23d, int64_t nel, void* stream) {
   // lx = 8 only: the roofline probe for the headline configuration
   using C = TCfg<8>;
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(ax_stream_probe<8>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "axhelm_probe_stream");
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ax_stream_probe<8>, C::NT, C::SMEM);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  static DevCache occ;
+  int blocks_per_sm = 0;
+  cudaError_t e = ctas_per_sm(occ, ax_stream_probe<8>, C::NT, C::SMEM, &blocks_per_sm);
+  if (e != cudaSuccess) return cuda_status(e, "axhelm_probe_stream");
   AxPtrs A{wd, ud, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
            h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   int64_t grid = (int64_t)blocks_per_sm * num_sms();

@@ -365,7 +365,7 @@ static cudaError_t ax_dot(const AxPtrs& A, int64_t nel, int lx, int mode, double
     }
     return e;
   }
-  e = launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
+  e = launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
   if (e == cudaSuccess) {
     const int nb = red_blocks(n);
     dot_kernel<<<nb, RT, 0, st>>>(A.u, A.w, nullptr, n, partial);
@@ -433,11 +433,21 @@ int axhelm_apply_box(double* wd, const double* ud, const double* dxd, const doub
                      const double* h1d, const double* g11d, const double* g22d, const double* g33d,
                      const double* g12d, const double* g13d, const double* g23d, int nx, int64_t nel,
                      int lx, int mode, double* partial, double* dot_out, int* xfolded, void* stream) {
+  // wd must start at an x-run start (ex = 0): the x-folding epilogue sums
+  // the faces shared by consecutive elements of each run of nx
   if (xfolded) *xfolded = 0;
   if (lx < 2 || lx > 16 || nel < 0 || nx < 1 || nel % nx != 0)
     return set_status(AXHELM_EINVAL, "axhelm_apply_box: bad sizes (nel must be whole x-runs of nx)");
+  const int keep = (mode & AXHELM_KEEP_W_L2) != 0;
+  mode &= ~AXHELM_KEEP_W_L2;
   if (mode != AXHELM_STRICT && mode != AXHELM_FAST)
     return set_status(AXHELM_EINVAL, "axhelm_apply_box: unknown mode %d", mode);
+  {
+    const double* ptrs[15] = {wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd,
+                              h1d, g11d, g22d, g33d, g12d, g13d, g23d};
+    for (int q = 0; q < 15; ++q)
+      if (!ptrs[q]) return set_status(AXHELM_EINVAL, "axhelm_apply_box: argument %d is NULL", q);
+  }
   if (dot_out && !partial) return set_status(AXHELM_EINVAL, "axhelm_apply_box: dot needs partial scratch");
   cudaStream_t st = (cudaStream_t)stream;
   if (nel == 0) {
@@ -446,10 +456,11 @@ int axhelm_apply_box(double* wd, const double* ud, const double* dxd, const doub
   }
   AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   AxExt X;
+  X.keep_w = keep;
   const char* xf_env = getenv("AXHELM_XFOLD");
   if (nx > 1 && lx > 2 && !(xf_env && xf_env[0] == '0') && dmma8_selected(A, lx, mode)) X.xrun = nx;
   cudaError_t e = dot_out ? ax_dot(A, nel, lx, mode, partial, dot_out, st, X)
-                          : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
+                          : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
   if (e == cudaSuccess && xfolded) *xfolded = X.xrun > 0;
   return cuda_status(e, "axhelm_apply_box");
 }
@@ -491,7 +502,15 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     X.lay = lay;
     // only the lx = 8 DMMA kernel publishes progress (its dot is fused, taken
     // before the follower assembles w); everything else runs sequentially
-    if (l1 > l0 && progress_capable(A, lx) && dmma8_selected(A, lx, mode)) {
+    // Co-residency assumption: the follower spins on counters the apply
+    // publishes, so every apply CTA must be able to become resident while
+    // follower CTAs occupy SMs.  The apply's persistent grid is sized by its
+    // own occupancy and the follower takes only registers / threads it
+    // leaves free; under an MPS SM limit (or another tenant) that no longer
+    // holds, so the schedule falls back to sequential there.
+    const char* mps = getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE");
+    const bool sm_limited = mps && atoi(mps) > 0 && atoi(mps) < 100;
+    if (l1 > l0 && !sm_limited && progress_capable(A, lx) && dmma8_selected(A, lx, mode)) {
       FollowStreams* fs = follow_streams();
       if (!fs) return set_status(AXHELM_ECUDA, "axhelm_ax_gs_box: cannot create the follower stream");
       // The apply is enqueued first and never waits on the follower, so it
@@ -503,7 +522,7 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
       if (e == cudaSuccess) e = cudaStreamWaitEvent(fs->side, fs->fork, 0);
       if (e == cudaSuccess)
         e = dot_out ? ax_dot(A, (l1 - l0) * lay, lx, mode, partial, dot_out, st, X)
-                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
+                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st, nullptr, nullptr, X);
       if (e == cudaSuccess) e = gs_box_follow(wd, nx, ny, lx, ez0, ez1, zlo, zhi, progress, l0, l1, fs->side);
       if (e == cudaSuccess) e = cudaEventRecord(fs->join, fs->side);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(st, fs->join, 0);
@@ -530,7 +549,7 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     X.xrun = xfold ? nx : 0;
     const int64_t nel = (b - a) * lay;
     e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st, X)
-                : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, nullptr, nullptr, X);
+                : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
     if (e != cudaSuccess) break;
     // planes whose every copy is computed: below layer ez0 + b, or all when
     // the layers above l1 are done by the caller

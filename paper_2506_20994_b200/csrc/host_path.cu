@@ -194,7 +194,12 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
   }
   const int64_t L3 = (int64_t)lx * lx * lx;
 
-  if (all_dev) {  // plain device call: run on the legacy default stream, synchronously
+  if (all_dev) {
+    // plain device call, synchronous like the reference's CPU kernel: wait for
+    // every stream of the device first (the caller may have produced the
+    // buffers on any stream, blocking or not), then run on the legacy stream
+    cudaError_t e0 = cudaDeviceSynchronize();
+    if (e0 != cudaSuccess) return cuda_status(e0, "__dace_ax_helm (device)");
     AxPtrs A{const_cast<double*>(ptrs[0]), ptrs[1], ptrs[2], ptrs[3], ptrs[4], ptrs[5],
              ptrs[6], ptrs[7], ptrs[8], ptrs[9], ptrs[10], ptrs[11], ptrs[12], ptrs[13],
              ptrs[14]};
@@ -297,9 +302,7 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
              f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
     const double* hz = kind[4] != DEV ? ptrs[4] : nullptr;   // dzd
     const double* hzt = kind[7] != DEV ? ptrs[7] : nullptr;  // dztd
-    const double* hx = kind[2] != DEV ? ptrs[2] : nullptr;   // dxd
-    const double* hxt = kind[5] != DEV ? ptrs[5] : nullptr;  // dxtd
-    if ((e = launch_ax(A, ne, lx, mode, S.st[s], hz, hzt, hx, hxt)) != cudaSuccess)
+    if ((e = launch_ax(A, ne, lx, mode, S.st[s], hz, hzt)) != cudaSuccess)
       return cuda_status(e, "__dace_ax_helm (kernel)");
     if (kind[0] == PINNED &&
         (e = cudaMemcpyAsync(const_cast<double*>(ptrs[0]) + off, f[0], bytes, cudaMemcpyDeviceToHost,

@@ -139,6 +139,9 @@ def test_tensorfile_golden_and_roundtrip(golden_dir, tmp_path):
     bad.write_bytes(blob[:-8])
     with pytest.raises(ParseError, match="3 of 4"):
         tensorfile.read_tensor(bad)
+    # a scalar is written as rank 1 (the reference's np.ascontiguousarray promotes 0-d)
+    tensorfile.write_tensor(p, np.float64(2.5))
+    assert p.read_bytes()[4:6] == bytes([1, 1]) and tensorfile.read_tensor(p).shape == (1,)
     s = tmp_path / "sizes.txt"
     tensorfile.write_sizes(s, 64, 8)
     assert s.read_text() == "64 8\n" and tensorfile.read_sizes(s) == (64, 8)

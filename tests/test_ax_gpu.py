@@ -350,3 +350,81 @@ def test_misaligned_device_buffers(torch, kern, lx, nel):
             assert o.digest(got) == o.digest(want)
         else:
             assert o.normwise_rel(got, want) <= FAST_TOL
+
+
+@pytest.mark.parametrize("lx", [6, 10])
+def test_graph_capture_on_unseen_matrix_pointer(torch, lx):
+    """axhelm_apply is purely stream-ordered (include/axhelm.h): capturing it
+    into a CUDA graph on matrices the library has never seen (no warm-up
+    call, so the host matrix cache misses inside the capture) must work and
+    replay bit-exact.  Round 1 synchronised the stream on such a miss."""
+    from paper_2506_20994_b200 import kernelrt
+
+    nel = 37
+    arrays = o.problem(lx, nel, seed=11)
+    want = o.ax(arrays)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
+    for name in o.MATRICES:  # fresh allocations: pointers no earlier test used
+        dev[name] = dev[name].clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        kernelrt.apply(dev, nel, lx, mode="strict")
+    dev["wd"].fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(dev["wd"].cpu().numpy(), want)
+    # later eager calls (cache now filled asynchronously) agree bit for bit
+    for _ in range(3):
+        dev["wd"].fill_(float("nan"))
+        kernelrt.apply(dev, nel, lx, mode="strict")
+        torch.cuda.synchronize()
+        assert np.array_equal(dev["wd"].cpu().numpy(), want)
+
+
+def test_concurrent_reference_symbol_calls(torch):
+    """callers may invoke the kernel from any thread (not on
+    overlapping outputs).  Three threads drive __dace_ax_helm at once (host
+    and device buffers, different lx), each result bit-exact."""
+    import ctypes
+    import threading
+
+    from paper_2506_20994_b200 import _lib
+
+    lib = ctypes.CDLL(str(_lib.lib_path()))
+    fn = lib.__dace_ax_helm
+    fn.restype = None
+    fn.argtypes = [ctypes.c_void_p] * 15 + [ctypes.c_int, ctypes.c_int]
+    assert lib.axhelm_get_mode() == 0  # strict default
+    jobs = []
+    for lx, nel, on_dev in ((8, 300, False), (11, 40, True), (5, 900, False)):
+        arrays = o.problem(lx, nel, seed=lx)
+        want = o.ax(arrays)
+        if on_dev:
+            bufs = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
+            ptrs = [bufs[n].data_ptr() for n in o.ABI_ORDER]
+        else:
+            bufs = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
+            ptrs = [bufs[n].ctypes.data for n in o.ABI_ORDER]
+        jobs.append((lx, nel, on_dev, bufs, ptrs, want))
+    torch.cuda.synchronize()
+    errors = []
+
+    def run(job):
+        lx, nel, on_dev, bufs, ptrs, want = job
+        try:
+            for _ in range(5):
+                fn(*ptrs, nel, lx)
+                got = bufs["wd"].cpu().numpy() if on_dev else bufs["wd"]
+                if not np.array_equal(got, want):
+                    errors.append(f"lx={lx} differs")
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
