@@ -35,3 +35,44 @@ def test_bench_defaults_are_the_headline_configuration():
 
     assert bench.LX == 8 and bench.NEL == 1 << 18 and bench.BYTES_PER_POINT == 72
     assert bench.flops_model(8, 32768) == 1_912_602_624  # frozen (reference tests/test_oracle.py:245)
+
+
+def test_self_launch_runs_n_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under
+    torch.distributed.run with 2 ranks (gloo here: no GPU); --dry-run stops
+    after the rank plumbing and rank 0 reports n_gpus = 2."""
+    import os
+    import subprocess
+
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"],
+                         env=env, capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["dry_run"] and sorted(d["ranks"]) == [0, 1]
+    assert d["launcher"] == "torch.distributed.run"
+
+
+def test_reference_problem_is_the_references_own_inputs():
+    """bench.reference_problem (chunk-parallel, PCG64 advanced per chunk)
+    reproduces mdg.bench._problem bit for bit (reference bench.py:41-47)."""
+    import numpy as np
+    import pytest
+
+    ref = Path("/root/reference/pkg/src")
+    if not ref.exists():
+        pytest.skip("reference sources not present")
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ref))
+    import bench
+    from mdg import bench as mbench
+
+    for lx, nel in ((8, 700), (5, 333), (12, 9)):
+        _, want = mbench._problem(lx, nel)
+        got = bench.reference_problem(nel, lx, chunk=128)
+        for k in bench.ABI:
+            assert np.array_equal(got[k], want[k]), (lx, nel, k)
