@@ -422,11 +422,11 @@ def pcg(arrays: dict[str, np.ndarray], gid: np.ndarray, mask: np.ndarray, f: np.
     for _ in range(iters):
         w = A(p)
         pw = float(np.sum(minv * p * w))
-        alpha = rz / pw
+        alpha = rz / pw if pw != 0.0 else 0.0  # exact convergence: step 0 (cg.cu cg_ratio)
         x = x + alpha * p
         r = r - alpha * mask * w
         rz_new = float(np.sum(minv * r * dinv * r))
         hist.append(float(np.sum(minv * r * r)))
-        p = dinv * r + (rz_new / rz) * p
+        p = dinv * r + (rz_new / rz if rz != 0.0 else 0.0) * p
         rz = rz_new
     return x, np.array(hist)

@@ -18,6 +18,14 @@
 #include "ax_launch.h"
 #include "box_gs.cuh"
 
+namespace {
+// CG step ratios with exact convergence handled: when the solve has
+// converged to an exactly zero residual (tiny problems), p.Ap or rz becomes
+// 0 and the textbook a / b would turn x into NaN; the step is 0 instead, so
+// further iterations leave x unchanged.
+__device__ __forceinline__ double cg_ratio(double a, double b) { return b != 0.0 ? a / b : 0.0; }
+}  // namespace
+
 namespace axb {
 
 constexpr int RT = 256;  // reduction block size
@@ -93,7 +101,7 @@ __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
                                  const double* __restrict__ dinv, const double* __restrict__ cwt,
                                  const double* __restrict__ sc, int64_t n,
                                  double* __restrict__ partial) {
-  const double alpha = sc[0] / sc[1];
+  const double alpha = cg_ratio(sc[0], sc[1]);
   double v[2] = {0.0, 0.0};
   for (int64_t q = (int64_t)blockIdx.x * RT + threadIdx.x; q < n; q += (int64_t)gridDim.x * RT) {
     x[q] = fma(alpha, p[q], x[q]);
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(RT, MINB) cg_update_box_kernel(double* __restr
   const int64_t DY = (int64_t)M.nx * L3 - n1 * LX;
   const int64_t DZ = (int64_t)M.nx * M.ny * L3 - n1 * L2;
   const int nl = (int)(M.ez1 - M.ez0);
-  const double alpha = a[0] / a[1];
+  const double alpha = cg_ratio(a[0], a[1]);
   double v[2] = {0.0, 0.0};
   for (int64_t e0 = (int64_t)blockIdx.x * EPI; e0 < nel; e0 += (int64_t)gridDim.x * EPI) {
     double c8[NP][8], rq[NP], dq[NP], cw[NP];
@@ -216,8 +224,8 @@ __global__ void cg_xpupdate_kernel(double* __restrict__ x, double* __restrict__ 
                                    const double* __restrict__ r, const double* __restrict__ dinv,
                                    const double* __restrict__ a, const double* __restrict__ sc_new,
                                    int64_t n) {
-  const double alpha = a[0] / a[1];
-  const double beta = sc_new[0] / a[0];
+  const double alpha = cg_ratio(a[0], a[1]);
+  const double beta = cg_ratio(sc_new[0], a[0]);
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     const double pq = p[q];
@@ -230,7 +238,7 @@ __global__ void cg_xpupdate_kernel(double* __restrict__ x, double* __restrict__ 
 __global__ void cg_pupdate_kernel(double* __restrict__ p, const double* __restrict__ r,
                                   const double* __restrict__ dinv, const double* __restrict__ sc_new,
                                   const double* __restrict__ sc_old, int64_t n) {
-  const double beta = sc_new[0] / sc_old[0];
+  const double beta = cg_ratio(sc_new[0], sc_old[0]);
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x)
     p[q] = fma(beta, p[q], dinv[q] * r[q]);

@@ -240,3 +240,34 @@ def test_graph_replay_equals_eager(torch, mode):
         xg, hg = pcg.solve(f, iters=20, graph=True)
         torch.cuda.synchronize()
         assert torch.equal(hg, he) and torch.equal(xg, xe)
+
+
+def test_pcg_converges_to_reference_dense_solve(torch, golden_dir):
+    """f2 pinned to reference arithmetic: JacobiPCG on the assembled operator
+    converges to x = K_II^-1 f_I (K assembled from the reference's element
+    matrices, mdg.sem.dense_assemble; tests/golden/make_assembled_golden.py)
+    to 1e-9 of max|x| (800 iterations: the random SPD metric blocks make K
+    ill-conditioned), in both the fused and the separate-pass form."""
+    from paper_2506_20994_b200.cg import JacobiPCG
+    from paper_2506_20994_b200.mesh import BoxMesh
+    from paper_2506_20994_b200.operator import HelmholtzOperator
+
+    with np.load(golden_dir / "assembled_cases.npz") as z:
+        tags = sorted({k.split("/")[0] for k in z.files})
+        cases = [(tag, {k.split("/")[1]: z[k] for k in z.files if k.startswith(tag + "/")}) for tag in tags]
+    for tag, c in cases:
+        if np.count_nonzero(np.abs(c["x"]) > 0) <= 50:
+            continue  # tiny interior: CG terminates exactly (p.Ap = 0)
+        dims, lx = tag.split("_lx")
+        nx, ny, nz = (int(v) for v in dims.split("x"))
+        m = BoxMesh(nx, ny, nz, int(lx))
+        geom = {k: torch.from_numpy(c[k]).cuda() for k in ("h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d")}
+        for fused in (True, False):
+            op = HelmholtzOperator(m, torch, "cuda", mode="fast", geometry=geom)
+            pcg = JacobiPCG(op, fused=fused)
+            f = torch.from_numpy(c["f"]).cuda()
+            x, hist = pcg.solve(f, iters=800)  # random SPD metrics: ill-conditioned
+            torch.cuda.synchronize()
+            got = x.cpu().numpy()
+            err = np.abs(got - c["x"]).max() / np.abs(c["x"]).max()
+            assert err <= 1e-9, (tag, fused, err, float(hist[-1]))

@@ -175,3 +175,35 @@ class TestOperatorProperties:
     def test_mdgt_golden_bytes(self, golden_dir):
         blob = (golden_dir / "mdgt_2x2.t").read_bytes()
         assert o.mdgt_encode(np.array([[1.0, 2.0], [3.0, -0.5]])) == blob
+
+
+def _assembled_cases(golden_dir):
+    with np.load(golden_dir / "assembled_cases.npz") as z:
+        tags = sorted({k.split("/")[0] for k in z.files})
+        for tag in tags:
+            dims, lx = tag.split("_lx")
+            nx, ny, nz = (int(v) for v in dims.split("x"))
+            yield (nx, ny, nz, int(lx)), {k.split("/")[1]: z[k] for k in z.files if k.startswith(tag + "/")}
+
+
+def test_oracle_dssum_and_pcg_pinned_to_reference_assembly(golden_dir):
+    """f1/f2 parity anchor: the oracle's assembled operator dssum(ax(u)) and
+    its PCG reproduce the global stiffness assembled from the reference's
+    own element matrices (mdg.sem.dense_assemble, sem.py:340-364;
+    tests/golden/make_assembled_golden.py): w to 1e-12 normwise, the
+    converged x to 1e-9 of the dense solve."""
+    for (nx, ny, nz, lx), c in _assembled_cases(golden_dir):
+        gid = o.box_mesh_gid(nx, ny, nz, lx)
+        a, b = o.operator_matrices(o.gll(lx)[2])
+        arrays = {k: c[k] for k in ("h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d")}
+        arrays.update({"dxd": a, "dyd": a, "dzd": a, "dxtd": b, "dytd": b, "dztd": b})
+        arrays["ud"] = c["u"]
+        arrays["wd"] = np.zeros_like(c["u"])
+        w = o.dssum(o.ax(arrays), gid)
+        assert o.normwise_rel(w, c["w"]) <= 1e-12, (nx, ny, nz, lx)
+        mask = o.gs_boundary_mask(nx, ny, nz, lx)
+        # the NumPy PCG is slow (the GPU test covers every case); a 7-node
+        # interior converges exactly and breaks down (p.Ap = 0): w only
+        if lx <= 5 and np.count_nonzero(np.abs(c["x"]) > 0) > 50:
+            x, _ = o.pcg(arrays, gid, mask, c["f"], iters=150)
+            assert np.abs(x - c["x"]).max() <= 1e-9 * np.abs(c["x"]).max(), (nx, ny, nz, lx)
