@@ -52,19 +52,6 @@ int cuda_status(cudaError_t e, const char* where) {
 // count) are per device: cudaFuncSetAttribute applies to the current
 // device's context only, so a process driving several GPUs needs one entry
 // per device.  Entries are written once (idempotent, benign race).
-constexpr int kMaxDev = 64;
-static int cur_dev() {
-  int d = 0;
-  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return -1;
-  return d;
-}
-struct DevCache {
-  std::atomic<int> v[kMaxDev];
-  DevCache() {
-    for (auto& x : v) x.store(0, std::memory_order_relaxed);
-  }
-};
-
 // ---------------------------------------------------------------- launch
 
 template <int LX, bool FAST>
@@ -88,9 +75,10 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
 // pf (v2, L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
-// + k-split) or dmma (v6, FP64 tensor cores; fast mode, lx = 8).  Default
-// ("auto"): v6 for fast lx = 8, v4 for every other lx <= 15 (16-B aligned
-// fields), else v2.  (v3 = v4 without its refinements and v5 = row per
+// + k-split), dmma (v6, FP64 tensor cores; fast mode, lx = 8) or line (v11,
+// lx >= 9, both modes).  Default ("auto"): v6 for fast lx = 8, v11 for lx
+// 9..16 (strict: except 14 / 15, see line_selected), v4 for every other
+// lx <= 15 (16-B aligned fields), else v2.  (v3 = v4 without its refinements and v5 = row per
 // thread were measured and retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
 static int g_variant = [] {
@@ -99,6 +87,7 @@ static int g_variant = [] {
   if (v && !strcmp(v, "pf")) return 2;
   if (v && !strcmp(v, "tma2")) return 4;
   if (v && !strcmp(v, "dmma")) return 6;
+  if (v && !strcmp(v, "line")) return 11;
   return 0;  // auto
 }();
 static int g_pf = [] {
@@ -114,9 +103,9 @@ static int g_cta_cap = [] {
   const char* v = getenv("AXHELM_CTAS_PER_SM");
   return v ? atoi(v) : 0;
 }();
-static int cap_ctas(int b) { return (g_cta_cap > 0 && g_cta_cap < b) ? g_cta_cap : b; }
+int cap_ctas(int b) { return (g_cta_cap > 0 && g_cta_cap < b) ? g_cta_cap : b; }
 
-static int num_sms() {
+int num_sms() {
   const int dev = cur_dev();
   if (dev < 0) return 1;
   int n = g_num_sms.v[dev].load(std::memory_order_relaxed);
@@ -139,13 +128,12 @@ static int num_sms() {
 // kernel's shared-memory path; later launches use the copy once its event
 // has completed.  axhelm_apply therefore stays purely stream-ordered.
 struct MatEntry {
-  const double* dz = nullptr;
-  const double* dzt = nullptr;
+  const double* m[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int lx = 0;
   int dev = -1;
   bool ready = false;
   uint64_t used = 0;
-  double* h = nullptr;  // pinned: z at [0, 256), zt at [256, 512)
+  double* h = nullptr;  // pinned: matrix q at [q * 256, q * 256 + lx * lx)
   cudaEvent_t ev = nullptr;
 };
 static std::mutex g_mat_mu;
@@ -153,12 +141,12 @@ static MatEntry g_mat[16];
 static uint64_t g_mat_clock = 0;
 static int* g_stale = nullptr;  // mapped pinned host flag
 
-// *have = true: z / zt hold the matrices (parameter path); false: the
-// caller poisons the parameter copy and passes no stale flag, so the kernel
-// reads the device arrays (the verification fails unless the bits match,
-// in which case the copy is exact anyway).
-static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, const double* hzt,
-                                 cudaStream_t st, double* z, double* zt, int** stale, bool* have) {
+static const double* mat_ptr(const AxPtrs& A, int q) {
+  return q == 0 ? A.dx : q == 1 ? A.dy : q == 2 ? A.dz : q == 3 ? A.dxt : q == 4 ? A.dyt : A.dzt;
+}
+
+cudaError_t host_matrices(const AxPtrs& A, int lx, const double* const* hm, cudaStream_t st,
+                          double* out, int** stale, bool* have) {
   const size_t n = (size_t)lx * lx;
   std::lock_guard<std::mutex> lock(g_mat_mu);
   *have = false;
@@ -168,22 +156,26 @@ static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, cons
     if (e != cudaSuccess) return e;
     *g_stale = 0;
   }
-  if (hz && hzt) {  // caller's host copies (host-staged __dace_ax_helm)
-    memcpy(z, hz, n * sizeof(double));
-    memcpy(zt, hzt, n * sizeof(double));
+  if (hm && hm[0] && hm[1] && hm[2] && hm[3] && hm[4] && hm[5]) {  // caller's host copies
+    for (int q = 0; q < 6; ++q) memcpy(out + q * n, hm[q], n * sizeof(double));
     *stale = g_stale;
     *have = true;
     return cudaSuccess;
   }
   if (*(volatile int*)g_stale) {  // a kernel saw a changed matrix: drop every copy
-    for (auto& m : g_mat) m.dz = m.dzt = nullptr, m.ready = false;
+    for (auto& m : g_mat) {
+      for (auto& p : m.m) p = nullptr;
+      m.ready = false;
+    }
     *(volatile int*)g_stale = 0;
   }
   const int dev = cur_dev();
   MatEntry* hit = nullptr;
   MatEntry* lru = &g_mat[0];
   for (auto& m : g_mat) {
-    if (m.dz == A.dz && m.dzt == A.dzt && m.lx == lx && m.dev == dev) hit = &m;
+    bool same = m.lx == lx && m.dev == dev;
+    for (int q = 0; q < 6 && same; ++q) same = m.m[q] == mat_ptr(A, q);
+    if (same) hit = &m;
     if (m.used < lru->used) lru = &m;
   }
   if (hit && !hit->ready) {  // fetch in flight: ready once its event has completed
@@ -194,8 +186,7 @@ static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, cons
   }
   if (hit && hit->ready) {
     hit->used = ++g_mat_clock;
-    memcpy(z, hit->h, n * sizeof(double));
-    memcpy(zt, hit->h + 256, n * sizeof(double));
+    for (int q = 0; q < 6; ++q) memcpy(out + q * n, hit->h + q * 256, n * sizeof(double));
     *stale = g_stale;
     *have = true;
     return cudaSuccess;
@@ -206,20 +197,21 @@ static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, cons
   if (e != cudaSuccess) return e;
   if (cs != cudaStreamCaptureStatusNone) return cudaSuccess;  // no side effects inside a capture
   MatEntry& m = *lru;
-  if (!m.h && (e = cudaHostAlloc(&m.h, 512 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess) return e;
+  if (!m.h && (e = cudaHostAlloc(&m.h, 6 * 256 * sizeof(double), cudaHostAllocPortable)) != cudaSuccess)
+    return e;
   if (m.ev && m.dev != dev) {
     cudaEventDestroy(m.ev);  // events belong to the device they were created on
     m.ev = nullptr;
   }
   if (!m.ev && (e = cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
-  m.dz = m.dzt = nullptr;
+  for (auto& p : m.m) p = nullptr;
   m.ready = false;
-  if ((e = cudaMemcpyAsync(m.h, A.dz, n * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(m.h + 256, A.dzt, n * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-      (e = cudaEventRecord(m.ev, st)) != cudaSuccess)
-    return e;
-  m.dz = A.dz;
-  m.dzt = A.dzt;
+  for (int q = 0; q < 6; ++q)
+    if ((e = cudaMemcpyAsync(m.h + q * 256, mat_ptr(A, q), n * sizeof(double), cudaMemcpyDeviceToHost,
+                             st)) != cudaSuccess)
+      return e;
+  if ((e = cudaEventRecord(m.ev, st)) != cudaSuccess) return e;
+  for (int q = 0; q < 6; ++q) m.m[q] = mat_ptr(A, q);
   m.lx = lx;
   m.dev = dev;
   m.used = ++g_mat_clock;
@@ -229,10 +221,10 @@ static cudaError_t host_matrices(const AxPtrs& A, int lx, const double* hz, cons
 // fill the kernel's transposed parameter copies (zT[k][l] = dz[l][k]) or
 // poison them (shared-memory path, see host_matrices)
 template <int LX>
-static cudaError_t param_matrices(TParams<LX>& P, cudaStream_t st, const double* hz, const double* hzt) {
-  double z[LX * LX], zt[LX * LX];
+static cudaError_t param_matrices(TParams<LX>& P, cudaStream_t st, const double* const* hm) {
+  double m6[6 * LX * LX];
   bool have = false;
-  cudaError_t e = host_matrices(P.A, LX, hz, hzt, st, z, zt, &P.stale, &have);
+  cudaError_t e = host_matrices(P.A, LX, hm, st, m6, &P.stale, &have);
   if (e != cudaSuccess) return e;
   if (!have) {
     const long long bits = 0x7ff4deadbeef0001LL;
@@ -241,6 +233,8 @@ static cudaError_t param_matrices(TParams<LX>& P, cudaStream_t st, const double*
     for (int q = 0; q < LX * LX; ++q) P.zT[q] = P.ztT[q] = poison;
     return cudaSuccess;
   }
+  const double* z = m6 + 2 * LX * LX;
+  const double* zt = m6 + 5 * LX * LX;
   for (int l = 0; l < LX; ++l)
     for (int k = 0; k < LX; ++k) {
       P.zT[k * LX + l] = z[l * LX + k];
@@ -255,28 +249,8 @@ static int g_nks8 = [] {
   return (d >= 1 && d <= 4) ? d : 2;
 }();
 
-// resident CTAs per SM of `kern` at `smem` bytes, per device; sets the
-// max-dynamic-shared-memory attribute on first use on each device
-template <typename K>
-static cudaError_t ctas_per_sm(DevCache& cache, K kern, int nt, size_t smem, int* out) {
-  const int dev = cur_dev();
-  if (dev < 0) return cudaErrorInvalidDevice;
-  int b = cache.v[dev].load(std::memory_order_relaxed);
-  if (b == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, nt, smem);
-    if (e != cudaSuccess) return e;
-    b = cap_ctas(b > 0 ? b : 1);
-    cache.v[dev].store(b, std::memory_order_relaxed);
-  }
-  *out = b;
-  return cudaSuccess;
-}
-
 template <int LX, bool FAST, int NKS, int D = 2>
-static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
-                               const double* hzt) {
+static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm) {
   using C = T2Cfg<LX, NKS, D>;
   static DevCache occ;
   int blocks_per_sm = 0;
@@ -285,7 +259,7 @@ static cudaError_t launch_tma2(const AxPtrs& A, int64_t nel, cudaStream_t st, co
   TParams<LX> P;
   P.A = A;
   P.nel = nel;
-  if ((e = param_matrices<LX>(P, st, hz, hzt)) != cudaSuccess) return e;
+  if ((e = param_matrices<LX>(P, st, hm)) != cudaSuccess) return e;
   const int64_t groups = (nel + C::EPL - 1) / C::EPL;
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
   if (grid > groups) grid = groups;
@@ -390,9 +364,14 @@ static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 }
 
 template <int LX, bool FAST>
-static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* hz,
-                                  const double* hzt, const AxExt& X) {
+static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm,
+                                  const AxExt& X) {
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
+  if constexpr (LX >= 9) {
+    constexpr int M = FAST ? AXHELM_FAST : AXHELM_STRICT;
+    if ((g_variant == 11 && line_selected(A, LX, AXHELM_FAST)) || (g_variant == 0 && line_selected(A, LX, M)))
+      return launch_line(A, nel, LX, M, st, hm);
+  }
   if constexpr (LX <= 8) {
     if ((g_variant == 6 || g_variant == 0) && FAST && aligned16(A)) {
       if constexpr (LX == 8) return launch_dmma8(A, nel, st, X);
@@ -401,13 +380,13 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
   if constexpr (LX <= 15) {
     if ((g_variant >= 4 || g_variant == 0) && aligned16(A)) {
       if constexpr (LX == 8) {
-        if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hz, hzt);
-        if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hz, hzt);
+        if (g_nks8 == 1) return launch_tma2<LX, FAST, 1>(A, nel, st, hm);
+        if (g_nks8 == 4) return launch_tma2<LX, FAST, 4>(A, nel, st, hm);
       }
       // lx = 7 strict: the one-deep ring (5 CTAs per SM instead of 2) is 1.08x
       // faster; for fast mode and lx 4..6 the two depths are within noise
-      if constexpr (LX == 7 && !FAST) return launch_tma2<LX, FAST, 1, 1>(A, nel, st, hz, hzt);
-      return launch_tma2<LX, FAST, T2Shape<LX>::NKS, T2Shape<LX>::D>(A, nel, st, hz, hzt);
+      if constexpr (LX == 7 && !FAST) return launch_tma2<LX, FAST, 1, 1>(A, nel, st, hm);
+      return launch_tma2<LX, FAST, T2Shape<LX>::NKS, T2Shape<LX>::D>(A, nel, st, hm);
     }
   }
   if constexpr (LX == 8) {
@@ -419,18 +398,18 @@ static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st,
 
 template <int LX>
 static cudaError_t launch_lx(const AxPtrs& A, int64_t nel, int mode, cudaStream_t st,
-                             const double* hz, const double* hzt, const AxExt& X) {
-  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hz, hzt, X)
-                             : launch_variant<LX, false>(A, nel, st, hz, hzt, X);
+                             const double* const* hm, const AxExt& X) {
+  return mode == AXHELM_FAST ? launch_variant<LX, true>(A, nel, st, hm, X)
+                             : launch_variant<LX, false>(A, nel, st, hm, X);
 }
 
 cudaError_t launch_ax(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
-                      const double* hz, const double* hzt, const AxExt& X) {
+                      const double* const* hm, const AxExt& X) {
   if (nel == 0) return cudaSuccess;
   switch (lx) {
 #define AXB_CASE(N) \
   case N:           \
-    return launch_lx<N>(A, nel, mode, st, hz, hzt, X);
+    return launch_lx<N>(A, nel, mode, st, hm, X);
     AXB_CASE(2) AXB_CASE(3) AXB_CASE(4) AXB_CASE(5) AXB_CASE(6) AXB_CASE(7)
     AXB_CASE(8) AXB_CASE(9) AXB_CASE(10) AXB_CASE(11) AXB_CASE(12)
     AXB_CASE(13) AXB_CASE(14) AXB_CASE(15) AXB_CASE(16)
@@ -477,7 +456,7 @@ int axhelm_apply(double* wd, const double* ud, const double* dxd, const double* 
   AxPtrs A{wd, ud, dxd, dyd, dzd, dxtd, dytd, dztd, h1d, g11d, g22d, g33d, g12d, g13d, g23d};
   AxExt X;
   X.keep_w = keep;
-  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream, nullptr, nullptr, X),
+  return cuda_status(launch_ax(A, nel, lx, mode, (cudaStream_t)stream, nullptr, X),
                      "axhelm_apply");
 }
 

@@ -373,7 +373,7 @@ static cudaError_t ax_dot(const AxPtrs& A, int64_t nel, int lx, int mode, double
     }
     return e;
   }
-  e = launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
+  e = launch_ax(A, nel, lx, mode, st, nullptr, X);
   if (e == cudaSuccess) {
     const int nb = red_blocks(n);
     dot_kernel<<<nb, RT, 0, st>>>(A.u, A.w, nullptr, n, partial);
@@ -468,7 +468,7 @@ int axhelm_apply_box(double* wd, const double* ud, const double* dxd, const doub
   const char* xf_env = getenv("AXHELM_XFOLD");
   if (nx > 1 && lx > 2 && !(xf_env && xf_env[0] == '0') && dmma8_selected(A, lx, mode)) X.xrun = nx;
   cudaError_t e = dot_out ? ax_dot(A, nel, lx, mode, partial, dot_out, st, X)
-                          : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
+                          : launch_ax(A, nel, lx, mode, st, nullptr, X);
   if (e == cudaSuccess && xfolded) *xfolded = X.xrun > 0;
   return cuda_status(e, "axhelm_apply_box");
 }
@@ -530,7 +530,7 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
       if (e == cudaSuccess) e = cudaStreamWaitEvent(fs->side, fs->fork, 0);
       if (e == cudaSuccess)
         e = dot_out ? ax_dot(A, (l1 - l0) * lay, lx, mode, partial, dot_out, st, X)
-                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st, nullptr, nullptr, X);
+                    : launch_ax(A, (l1 - l0) * lay, lx, mode, st, nullptr, X);
       if (e == cudaSuccess) e = gs_box_follow(wd, nx, ny, lx, ez0, ez1, zlo, zhi, progress, l0, l1, fs->side);
       if (e == cudaSuccess) e = cudaEventRecord(fs->join, fs->side);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(st, fs->join, 0);
@@ -557,7 +557,7 @@ int axhelm_ax_gs_box(double* wd, const double* ud, const double* dxd, const doub
     X.xrun = xfold ? nx : 0;
     const int64_t nel = (b - a) * lay;
     e = dot_out ? ax_dot(A, nel, lx, mode, partial, chunk_dot + nchunks, st, X)
-                : launch_ax(A, nel, lx, mode, st, nullptr, nullptr, X);
+                : launch_ax(A, nel, lx, mode, st, nullptr, X);
     if (e != cudaSuccess) break;
     // planes whose every copy is computed: below layer ez0 + b, or all when
     // the layers above l1 are done by the caller

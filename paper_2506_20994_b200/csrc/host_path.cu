@@ -300,9 +300,9 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
     }
     AxPtrs A{const_cast<double*>(f[0]), f[1], mat[0], mat[1], mat[2], mat[3], mat[4], mat[5],
              f[2], f[3], f[4], f[5], f[6], f[7], f[8]};
-    const double* hz = kind[4] != DEV ? ptrs[4] : nullptr;   // dzd
-    const double* hzt = kind[7] != DEV ? ptrs[7] : nullptr;  // dztd
-    if ((e = launch_ax(A, ne, lx, mode, S.st[s], hz, hzt)) != cudaSuccess)
+    const double* hm[6];  // host copies of dxd .. dztd (when they are host arrays)
+    for (int q = 0; q < 6; ++q) hm[q] = kind[2 + q] != DEV ? ptrs[2 + q] : nullptr;
+    if ((e = launch_ax(A, ne, lx, mode, S.st[s], hm)) != cudaSuccess)
       return cuda_status(e, "__dace_ax_helm (kernel)");
     if (kind[0] == PINNED &&
         (e = cudaMemcpyAsync(const_cast<double*>(ptrs[0]) + off, f[0], bytes, cudaMemcpyDeviceToHost,

@@ -205,18 +205,20 @@ def test_full_size_sampled_elements_bit_exact(torch, kern):
     assert torch.equal(dev["wd"], 2.0 * w1)
 
 
-def test_matrix_changed_in_place_is_honoured(torch, kern):
-    """The library caches host copies of the t-direction matrices keyed by
-    device pointer; a matrix rewritten in place (same pointer, new values)
-    must still be the one applied (the kernel verifies its copy)."""
-    lx, nel = 8, 300
+@pytest.mark.parametrize("lx", [8, 12])
+def test_matrix_changed_in_place_is_honoured(torch, kern, lx):
+    """The library caches host copies of the matrices keyed by device
+    pointer (v4: dz / dzt, v11 line kernel: all six); a matrix rewritten in
+    place (same pointer, new values) must still be the one applied (the
+    kernel verifies its copy)."""
+    nel = 300
     arrays = o.problem(lx, nel)
     dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in arrays.items()}
     kern["strict"](dev, nel, lx)
     torch.cuda.synchronize()
     assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays))
     rng = np.random.default_rng(8)
-    for name in ("dzd", "dztd", "dxd"):
+    for name in ("dzd", "dztd", "dxd", "dyd", "dxtd", "dytd"):
         new = rng.standard_normal((lx, lx))
         arrays[name] = new
         dev[name].copy_(torch.from_numpy(new))
@@ -225,6 +227,51 @@ def test_matrix_changed_in_place_is_honoured(torch, kern):
             kern["strict"](dev, nel, lx)
             torch.cuda.synchronize()
             assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays)), name
+
+
+@pytest.mark.parametrize("lx", range(9, 17))
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_line_kernel_many_iterations(torch, kern, lx, mode):
+    """v11 line kernel (lx 9..16): several elements per persistent CTA (the u
+    buffer re-armed by TMA after stage 1, the mbarrier parity flipping, the
+    geometry pipeline and L2 prefetch crossing elements), odd element
+    offsets for odd lx^3 and the past-the-end fallback element — strict
+    bit-exact, fast within 1e-12."""
+    nel = 2600 if lx <= 12 else 1300
+    arrays = o.problem(lx, nel, seed=5 + lx)
+    want = o.ax(arrays)
+    got = run_dev(torch, kern[mode], arrays, nel, lx)
+    if mode == "strict":
+        assert o.digest(got) == o.digest(want), lx
+    else:
+        assert o.normwise_rel(got, want) <= FAST_TOL, lx
+
+
+@pytest.mark.parametrize("lx", [9, 12, 16])
+def test_line_kernel_geometry_and_w_misaligned(torch, kern, lx):
+    """The line kernel needs only u 16-B aligned (its TMA operand); h1, the
+    six G fields and w are plain coalesced loads / stores, so 8-B-offset
+    views of those must still take it and give the same bits."""
+    nel = 77
+    arrays = o.problem(lx, nel, seed=3)
+    want = o.ax(arrays)
+    for mode in ("strict", "fast"):
+        dev = {}
+        for k, v in arrays.items():
+            if v.ndim == 4 and k != "ud":
+                flat = torch.empty(v.size + 1, dtype=torch.float64, device="cuda")
+                dev[k] = flat[1:].view(v.shape)
+                dev[k].copy_(torch.from_numpy(np.ascontiguousarray(v)))
+            else:
+                dev[k] = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        dev["wd"].fill_(np.nan)
+        kern[mode](dev, nel, lx)
+        torch.cuda.synchronize()
+        got = dev["wd"].cpu().numpy()
+        if mode == "strict":
+            assert o.digest(got) == o.digest(want)
+        else:
+            assert o.normwise_rel(got, want) <= FAST_TOL
 
 
 @pytest.mark.parametrize("lx", [9, 10, 11, 12])
@@ -323,7 +370,7 @@ def test_pageable_host_path_large_bit_exact(torch, kern):
     assert np.array_equal(host["wd"], want)
 
 
-@pytest.mark.parametrize("lx,nel", [(8, 37), (5, 41), (10, 9), (7, 12), (2, 101)])
+@pytest.mark.parametrize("lx,nel", [(8, 37), (5, 41), (10, 9), (7, 12), (2, 101), (12, 9), (13, 7)])
 def test_misaligned_device_buffers(torch, kern, lx, nel):
     """Field buffers 8 B off a 16-B boundary (views into a larger allocation,
     as a caller slicing its own arena would pass): the 16-B TMA / DMMA paths
@@ -352,7 +399,7 @@ def test_misaligned_device_buffers(torch, kern, lx, nel):
             assert o.normwise_rel(got, want) <= FAST_TOL
 
 
-@pytest.mark.parametrize("lx", [6, 10])
+@pytest.mark.parametrize("lx", [6, 10, 12])
 def test_graph_capture_on_unseen_matrix_pointer(torch, lx):
     """axhelm_apply is purely stream-ordered (include/axhelm.h): capturing it
     into a CUDA graph on matrices the library has never seen (no warm-up
