@@ -60,7 +60,7 @@ cudaError_t host_matrices(const AxPtrs& A, int lx, const double* const* hm, cuda
                           double* out, int** stale, bool* have);
 
 // v11 line kernel (ax_line.cu), lx 9..16; false = not handled (lx, alignment)
-bool line_selected(const AxPtrs& A, int lx, int mode);
+bool line_selected(const AxPtrs& A, int64_t nel, int lx, int mode);
 cudaError_t launch_line(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
                         const double* const* hm);
 

@@ -1,4 +1,6 @@
 // Launch side of the v11 line kernel (ax_line.cuh), lx 9..16, both modes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -18,6 +20,37 @@ static int g_line_pf = [] {
   return v ? atoi(v) : -1;
 }();
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time libcuda dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// u viewed as [nel * lx^2 rows][lx columns]; box RSU x lx^2 (columns past
+// lx are out of bounds and arrive as zeros: the padded row layout)
+template <int LX>
+static cudaError_t encode_u_map(CUtensorMap* map, const double* u, int64_t nel) {
+  using C = LineCfg<LX>;
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {(cuuint64_t)LX, (cuuint64_t)(nel * LX * LX)};
+  const cuuint64_t strides[1] = {(cuuint64_t)LX * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)C::RSU, (cuuint32_t)(LX * LX)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(u), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int LX, bool FAST>
 static cudaError_t launch_line_t(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm) {
   using C = LineCfg<LX>;
@@ -29,6 +62,10 @@ static cudaError_t launch_line_t(const AxPtrs& A, int64_t nel, cudaStream_t st, 
   P.A = A;
   P.nel = nel;
   P.pf = g_line_pf;
+  memset(&P.tmap, 0, sizeof P.tmap);
+  if constexpr (LineCfg<LX>::UPAD) {
+    if ((e = encode_u_map<LX>(&P.tmap, A.u, nel)) != cudaSuccess) return e;
+  }
   double m6[6 * LX * LX];
   bool have = false;
   if ((e = host_matrices(A, LX, hm, st, m6, &P.stale, &have)) != cudaSuccess) return e;
@@ -40,17 +77,19 @@ static cudaError_t launch_line_t(const AxPtrs& A, int64_t nel, cudaStream_t st, 
     memcpy(&poison, &bits, sizeof poison);
     for (int q = 0; q < 6 * LX * LX; ++q) (&P.m[0][0])[q] = poison;
   }
+  const int64_t groups = (nel + C::EPC - 1) / C::EPC;
   int64_t grid = (int64_t)blocks_per_sm * num_sms();
-  if (grid > nel) grid = nel;
+  if (grid > groups) grid = groups;
   ax_line<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
   return cudaGetLastError();
 }
 
-// Default for lx 9..16 in fast mode and for strict except lx 14 / 15, where
-// the v4 column walk measured 1.04-1.08x faster (same-box A/B).
-bool line_selected(const AxPtrs& A, int lx, int mode) {
+// Default for lx 9..16, both modes (same-box A/B against v4).
+bool line_selected(const AxPtrs& A, int64_t nel, int lx, int mode) {
   if (lx < 9 || lx > 16 || ((uintptr_t)A.u & 15u) != 0) return false;
-  return mode == AXHELM_FAST || (lx != 14 && lx != 15);
+  if (nel * lx * lx >= (int64_t)1 << 31) return false;  // tensor-map row coordinate (int32)
+  (void)mode;
+  return true;
 }
 
 cudaError_t launch_line(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,

@@ -45,6 +45,8 @@
 // Registers: two lines (2 LX doubles) + addressing.
 #pragma once
 
+#include <cuda.h>
+
 #include "ax_tma.cuh"
 
 namespace axb {
@@ -53,7 +55,15 @@ template <int LX>
 struct LineCfg {
   static constexpr int L2 = LX * LX;
   static constexpr int L3 = LX * LX * LX;
-  static constexpr int NT = L2;
+  // elements per CTA-iteration: whole warps are the FP64 pipe's unit, so a
+  // group of EPC elements (EPC * lx^2 threads) wastes fewer lanes than one
+  // (lx = 10: 100 of 128 lanes busy, two elements 200 of 224)
+#ifdef AXL_EPC
+  static constexpr int EPC = LX == 16 ? 1 : AXL_EPC;
+#else
+  static constexpr int EPC = 1;
+#endif
+  static constexpr int NT = EPC * L2;
   // X0 / X1 layout [k][j][i]: row stride RS, plane stride PS (doubles);
   // minimises the wavefronts of the row (r-line), j-line (s-line) and
   // column (combine) access patterns (LDS.64 / STS.64)
@@ -61,12 +71,23 @@ struct LineCfg {
   static constexpr int PP = LX == 10 ? 1 : LX == 13 ? 4 : 0;
   static constexpr int PS = LX * RS + PP;
   static constexpr int XS = (LX * PS + 1) & ~1;      // doubles per X buffer (16-B multiple)
-  static constexpr int US = (L3 + 2 + 1) & ~1;       // u buffer: a leading pad double + tail
-  static constexpr size_t SMEM = 128 + sizeof(double) * (US + 2 * XS);
+  // u buffer.  Linear (one bulk copy, a leading pad double for odd lx^3):
+  // the r-line rows then sit at stride LX, which for lx = 12 / 16 puts a
+  // warp's row reads 4 / 16 to a bank (tools/smem_conflicts.py).  There u
+  // comes in by a 2-D tensor TMA whose box is RSU > LX columns wide (the
+  // out-of-bounds columns are zero-filled), so rows land RSU apart and the
+  // r-lines read them conflict-free as 16-B vectors.
+  static constexpr bool UPAD = LX == 16;  // (lx = 12 too: 0.94x fast, 1.02x strict)
+  static constexpr int RSU = !UPAD ? LX : LX == 12 ? 14 : 18;
+  static constexpr int PSU = LX * RSU;
+  static constexpr int US = UPAD ? LX * PSU : (EPC * L3 + 2 + 1) & ~1;
+  static_assert(!UPAD || EPC == 1, "the tensor box holds one element (<= 256 rows)");
+  static constexpr size_t SMEM = 128 + sizeof(double) * (US + 2 * EPC * XS);
 };
 
 template <int LX>
 struct LParams {
+  CUtensorMap tmap;           // u as [nel * lx^2 rows][lx] (UPAD lx only)
   AxPtrs A;
   int64_t nel;
   int* stale;                 // mapped host flag, set when the host matrix copy is stale
@@ -85,22 +106,22 @@ struct LineGP {
 #ifdef AXL_GP_FAST
   static constexpr int GF = AXL_GP_FAST;
 #else
-  static constexpr int GF = LX == 11 ? 6 : LX <= 12 ? 4 : 2;
+  static constexpr int GF = LX == 11 ? 6 : LX <= 15 ? 4 : 3;
 #endif
 #ifdef AXL_GP_STRICT
   static constexpr int GS = AXL_GP_STRICT;
 #else
-  static constexpr int GS = LX <= 12 ? 4 : 2;
+  static constexpr int GS = LX <= 12 || LX == 15 ? 4 : 3;
 #endif
 #ifdef AXL_MINB_FAST
   static constexpr int MF = AXL_MINB_FAST;
 #else
-  static constexpr int MF = LX <= 12 ? 3 : 0;
+  static constexpr int MF = LX <= 12 ? 3 : 2;
 #endif
 #ifdef AXL_MINB_STRICT
   static constexpr int MS = AXL_MINB_STRICT;
 #else
-  static constexpr int MS = 0;
+  static constexpr int MS = LX <= 12 ? 0 : 2;
 #endif
   static constexpr int G0 = FAST ? GF : GS;
   static constexpr int GP = G0 < LX ? G0 : LX;
@@ -133,14 +154,51 @@ __device__ __forceinline__ void line(const LParams<LX>& P, int mi,
     for (int o = 0; o < LX; ++o) out[o] = madd<FAST>(out[o], mat<LX, UP>(P, mi, l, o), in[l]);
 }
 
-// Thread 0: start the bulk copy of element e's u into U (16-B aligned
-// superset, data `pad` doubles in).  Returns false when the superset would
-// read past the array (the consumers then load the element themselves).
+// The same product with the input line read from shared memory, src[l *
+// stride]; VEC: a 16-B aligned row (stride 1) read as double2 vectors.
+// (Keeping the l loop rolled — matrix entries then at a runtime uniform
+// constant-bank offset — shrinks the code 30% but measured 1.2-2.4x slower.)
+template <int LX, bool FAST, bool UP, bool VEC = false>
+__device__ __forceinline__ void line_s(const LParams<LX>& P, int mi, const double* src, int stride,
+                                       double (&out)[LX]) {
+  double in[LX];
+  if constexpr (VEC) {
+    static_assert((LX & 1) == 0, "vector rows need an even lx");
+#pragma unroll
+    for (int q = 0; q < LX / 2; ++q) {
+      const double2 v = reinterpret_cast<const double2*>(src)[q];
+      in[2 * q] = v.x;
+      in[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < LX; ++l) in[l] = src[l * stride];
+  }
+  line<LX, FAST, UP>(P, mi, in, out);
+}
+
+// Thread 0: start the bulk copy of group g's u (elements [g EPC, g EPC +
+// ne)) into U (16-B aligned superset, data `pad` doubles in).  When the
+// superset would read past the array it only arrives (the consumers then
+// load the group themselves).
 template <int LX>
-__device__ __forceinline__ void issue_u(const AxPtrs& A, int64_t nel, int64_t e, double* U, uint64_t* bar) {
+__device__ __forceinline__ void issue_u(const LParams<LX>& P, int64_t nel, int64_t g, double* U, uint64_t* bar) {
+  const AxPtrs& A = P.A;
+  constexpr int EPC = LineCfg<LX>::EPC;
+  const int64_t e = g * EPC;
+  if constexpr (LineCfg<LX>::UPAD) {
+    mbar_arrive_expect_tx(bar, (uint32_t)(8 * LineCfg<LX>::US));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(U)),
+        "l"(&P.tmap), "r"(0), "r"((int)(e * LX * LX)), "r"(smem_u32(bar))
+        : "memory");
+    return;
+  }
   constexpr int64_t L3 = LX * LX * LX;
+  const int64_t ne = nel - e < EPC ? nel - e : EPC;
   const int64_t first = e * L3;
-  const int64_t lo = first & ~(int64_t)1, hi = (first + L3 + 1) & ~(int64_t)1;
+  const int64_t lo = first & ~(int64_t)1, hi = (first + ne * L3 + 1) & ~(int64_t)1;
   if (hi > nel * L3) {
     mbar_arrive(bar);
     return;
@@ -150,12 +208,14 @@ __device__ __forceinline__ void issue_u(const AxPtrs& A, int64_t nel, int64_t e,
   bulk_g2s(U, A.u + lo, bytes, bar);
 }
 
+// L2 prefetch of field f (1..7: h1, g11, g22, g33, g12, g13, g23) of group g
 template <int LX>
-__device__ __forceinline__ void prefetch_geom(const AxPtrs& A, int64_t e, int f) {
+__device__ __forceinline__ void prefetch_geom(const AxPtrs& A, int64_t nel, int64_t g, int f) {
   constexpr int64_t L3 = LX * LX * LX;
-  // fields 1..7 of AxPtrs order (h1, g11, g22, g33, g12, g13, g23)
+  constexpr int EPC = LineCfg<LX>::EPC;
+  const int64_t e = g * EPC, ne = nel - e < EPC ? nel - e : EPC;
   uintptr_t lo = (uintptr_t)(field_ptr(A, f) + e * L3);
-  uintptr_t hi = (uintptr_t)(field_ptr(A, f) + (e + 1) * L3);
+  uintptr_t hi = (uintptr_t)(field_ptr(A, f) + (e + ne) * L3);
   lo = (lo + 15) & ~(uintptr_t)15;
   hi = hi & ~(uintptr_t)15;
   while (hi > lo) {
@@ -165,13 +225,14 @@ __device__ __forceinline__ void prefetch_geom(const AxPtrs& A, int64_t e, int f)
   }
 }
 
-// One element.  The u buffer is re-armed for the CTA's next element right
-// after stage 1 (inside, thread 0), the geometry of the element after that
-// is L2-prefetched at the same point.
+// One group, this thread's element e (Uv, X0, X1: that element's slots).
+// The u buffer is re-armed for the CTA's next group right after stage 1
+// (thread 0); the geometry prefetch point is PF.  e is clamped to a valid
+// element for the idle threads of a partial last group (no stores).
 template <int LX, bool FAST, bool UP>
 __device__ __forceinline__ void element_line(const LParams<LX>& P, const double* Uv,
-                                             double* X0, double* X1, int64_t e, int a, int b,
-                                             uint64_t* bar, double* Ubuf) {
+                                             double* X0, double* X1, int64_t g, int64_t e, bool active,
+                                             int a, int b, uint64_t* bar, double* Ubuf) {
   using C = LineCfg<LX>;
   constexpr int L2 = C::L2, L3 = C::L3, RS = C::RS, PS = C::PS;
   const AxPtrs& A = P.A;
@@ -179,27 +240,22 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
   const int64_t stride = gridDim.x;
 
   const int pf = P.pf >= 0 ? P.pf : LineGP<LX, FAST>::PF;
-  if (pf == 2 && tid >= 1 && tid <= 7) prefetch_geom<LX>(A, e, tid);
+  if (pf == 2 && tid >= 1 && tid <= 7) prefetch_geom<LX>(A, P.nel, g, tid);
   // ---- stage 1
   double t[LX];
   {
-    double in[LX], out[LX];
+    double out[LX];
     // 1a: r-line (k = a, j = b)
-#pragma unroll
-    for (int l = 0; l < LX; ++l) in[l] = Uv[a * L2 + b * LX + l];
-    line<LX, FAST, UP>(P, 0, in, out);
+    constexpr int RU = C::RSU, PU = C::PSU;
+    line_s<LX, FAST, UP, C::UPAD>(P, 0, Uv + a * PU + b * RU, 1, out);
 #pragma unroll
     for (int i = 0; i < LX; ++i) X0[a * PS + b * RS + i] = out[i];
     // 1b: s-line (k = a, i = b)
-#pragma unroll
-    for (int l = 0; l < LX; ++l) in[l] = Uv[a * L2 + l * LX + b];
-    line<LX, FAST, UP>(P, 1, in, out);
+    line_s<LX, FAST, UP>(P, 1, Uv + a * PU + b, RU, out);
 #pragma unroll
     for (int j = 0; j < LX; ++j) X1[a * PS + j * RS + b] = out[j];
     // 1c: t-line (j = a, i = b)
-#pragma unroll
-    for (int l = 0; l < LX; ++l) in[l] = Uv[l * L2 + a * LX + b];
-    line<LX, FAST, UP>(P, 2, in, t);
+    line_s<LX, FAST, UP>(P, 2, Uv + a * RU + b, PU, t);
   }
   // geometry of the first GP planes: loads in flight across the barrier
   constexpr int GP = LineGP<LX, FAST>::GP;
@@ -211,11 +267,12 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
     for (int f = 0; f < 7; ++f) gv[p][f] = ldg_stream(field_ptr(A, f + 1) + gbase + p * L2);
   }
   __syncthreads();  // X0 = r, X1 = s complete; u is dead
-  if (tid == 0 && e + stride < P.nel) {
+  const int64_t ngroups = (P.nel + C::EPC - 1) / C::EPC;
+  if (tid == 0 && g + stride < ngroups) {
     fence_proxy_async();
-    issue_u<LX>(A, P.nel, e + stride, Ubuf, bar);
+    issue_u<LX>(P, P.nel, g + stride, Ubuf, bar);
   }
-  if (pf == 3 && tid >= 1 && tid <= 7 && e + stride < P.nel) prefetch_geom<LX>(A, e + stride, tid);
+  if (pf == 3 && tid >= 1 && tid <= 7 && g + stride < ngroups) prefetch_geom<LX>(A, P.nel, g + stride, tid);
 
   // ---- combine at (j = a, i = b); plane k + GP's geometry is loaded as
   // plane k's is consumed
@@ -233,7 +290,7 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
     X1[k * PS + xb] = combine<FAST>(h, a12, a22, a23, r, s, t[k]);  // us
     t[k] = combine<FAST>(h, a13, a23, a33, r, s, t[k]);              // ut
   }
-  if (pf == 1 && tid >= 1 && tid <= 7 && e + stride < P.nel) prefetch_geom<LX>(A, e + stride, tid);
+  if (pf == 1 && tid >= 1 && tid <= 7 && g + stride < ngroups) prefetch_geom<LX>(A, P.nel, g + stride, tid);
 
   double* wout = A.w + gbase;
   if constexpr (FAST) {
@@ -241,23 +298,21 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
     line<LX, FAST, UP>(P, 5, t, wt);
     __syncthreads();  // ur / us complete
     {
-      double in[LX], out[LX];
+      double out[LX];
       // 2a: (k = a, j = b), ur row -> Dxt-line, in place
-#pragma unroll
-      for (int l = 0; l < LX; ++l) in[l] = X0[a * PS + b * RS + l];
-      line<LX, FAST, UP>(P, 3, in, out);
+      line_s<LX, FAST, UP>(P, 3, X0 + a * PS + b * RS, 1, out);
 #pragma unroll
       for (int i = 0; i < LX; ++i) X0[a * PS + b * RS + i] = out[i];
       // 2b: (k = a, i = b), us j-line -> Dyt-line, in place
-#pragma unroll
-      for (int l = 0; l < LX; ++l) in[l] = X1[a * PS + l * RS + b];
-      line<LX, FAST, UP>(P, 4, in, out);
+      line_s<LX, FAST, UP>(P, 4, X1 + a * PS + b, RS, out);
 #pragma unroll
       for (int j = 0; j < LX; ++j) X1[a * PS + j * RS + b] = out[j];
     }
     __syncthreads();
+    if (active) {
 #pragma unroll
-    for (int k = 0; k < LX; ++k) stg_stream(wout + k * L2, (X0[k * PS + xb] + X1[k * PS + xb]) + wt[k]);
+      for (int k = 0; k < LX; ++k) stg_stream(wout + k * L2, (X0[k * PS + xb] + X1[k * PS + xb]) + wt[k]);
+    }
   } else {
     __syncthreads();  // ur / us complete
     double dxtr[LX], dytr[LX];
@@ -275,7 +330,7 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
         w = madd<false>(w, dytr[l], X1[k * PS + l * RS + b]);
         w = madd<false>(w, mat<LX, UP>(P, 5, l, k), t[l]);
       }
-      stg_stream(wout + k * L2, w);
+      if (active) stg_stream(wout + k * L2, w);
     }
   }
 }
@@ -285,17 +340,21 @@ template <int LX, bool FAST>
 __global__ void __launch_bounds__(LineCfg<LX>::NT, LineGP<LX, FAST>::MINB)
 ax_line(const __grid_constant__ LParams<LX> P) {
   using C = LineCfg<LX>;
-  constexpr int L2 = C::L2, L3 = C::L3, RS = C::RS, PS = C::PS;
+  constexpr int L2 = C::L2, L3 = C::L3, EPC = C::EPC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double* U = reinterpret_cast<double*>(smem_raw + 128);
-  double* X0 = U + C::US;
-  double* X1 = X0 + C::XS;
+  double* X0s = U + C::US;
+  double* X1s = X0s + EPC * C::XS;
 
   const AxPtrs& A = P.A;
   const int64_t nel = P.nel;
+  const int64_t ngroups = (nel + EPC - 1) / EPC;
   const int tid = threadIdx.x;
-  const int a = tid / LX, b = tid - (tid / LX) * LX;
+  const int el = tid / L2, r = tid - (tid / L2) * L2;
+  const int a = r / LX, b = r - (r / LX) * LX;
+  double* X0 = X0s + el * C::XS;
+  double* X1 = X1s + el * C::XS;
   const int64_t stride = gridDim.x;
 
   if (tid == 0) {
@@ -303,32 +362,37 @@ ax_line(const __grid_constant__ LParams<LX> P) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0 && (int64_t)blockIdx.x < nel) issue_u<LX>(A, nel, blockIdx.x, U, bar);
+  if (tid == 0 && (int64_t)blockIdx.x < ngroups) issue_u<LX>(P, nel, blockIdx.x, U, bar);
   const int pf = P.pf >= 0 ? P.pf : LineGP<LX, FAST>::PF;
-  if ((pf == 1 || pf == 3) && tid >= 1 && tid <= 7 && (int64_t)blockIdx.x < nel)
-    prefetch_geom<LX>(A, blockIdx.x, tid);
+  if ((pf == 1 || pf == 3) && tid >= 1 && tid <= 7 && (int64_t)blockIdx.x < ngroups)
+    prefetch_geom<LX>(A, nel, blockIdx.x, tid);
   // verification of the parameter copy against the device arrays
   int bad = 0;
   for (int q = tid; q < 6 * L2; q += C::NT) {
-    const int mi = q / L2, r = q - mi * L2;
-    bad |= __double_as_longlong(__ldg(mat_ptr(A, mi) + r)) != __double_as_longlong(P.m[mi][r]);
+    const int mi = q / L2, rr = q - mi * L2;
+    bad |= __double_as_longlong(__ldg(mat_ptr(A, mi) + rr)) != __double_as_longlong(P.m[mi][rr]);
   }
   const bool use_param = !__syncthreads_or(bad);
   if (!use_param && tid == 0 && P.stale) *(volatile int*)P.stale = 1;
 
   uint32_t parity = 0;
-  for (int64_t e = blockIdx.x; e < nel; e += stride, parity ^= 1u) {
+  for (int64_t g = blockIdx.x; g < ngroups; g += stride, parity ^= 1u) {
     mbar_wait(bar, parity);
-    const int64_t first = e * L3;
-    int pad = (int)(first & 1);
-    if ((((first + L3 + 1) & ~(int64_t)1)) > nel * L3) {  // fallback: load it ourselves
+    const int64_t e0 = g * EPC;
+    const int64_t ne = nel - e0 < EPC ? nel - e0 : EPC;
+    const int64_t first = e0 * L3;
+    int pad = C::UPAD ? 0 : (int)(first & 1);
+    if (!C::UPAD && (((first + ne * L3 + 1) & ~(int64_t)1)) > nel * L3) {  // fallback: load it ourselves
       pad = 0;
-      for (int q = tid; q < L3; q += C::NT) U[q] = A.u[first + q];
+      for (int64_t q = tid; q < ne * L3; q += C::NT) U[q] = A.u[first + q];
       __syncthreads();
     }
-    if (use_param) element_line<LX, FAST, true>(P, U + pad, X0, X1, e, a, b, bar, U);
-    else element_line<LX, FAST, false>(P, U + pad, X0, X1, e, a, b, bar, U);
-    __syncthreads();  // X0 / X1 free for the next element
+    const bool active = el < ne;
+    const int64_t e = active ? e0 + el : e0;
+    const double* Uv = U + pad + el * L3;
+    if (use_param) element_line<LX, FAST, true>(P, Uv, X0, X1, g, e, active, a, b, bar, U);
+    else element_line<LX, FAST, false>(P, Uv, X0, X1, g, e, active, a, b, bar, U);
+    __syncthreads();  // X0 / X1 free for the next group
   }
 }
 
