@@ -332,7 +332,7 @@ def kernel_name(lx, mode):
     if v == "auto":
         if lx == 8 and mode == "fast":
             return "ax_dmma8 (FP64 DMMA m8n8k4, TMA ring)"
-        if lx >= 9:
+        if lx >= 9 or (lx == 7 and mode == "fast"):
             return f"ax_line<{lx},{mode}> (line contractions, constant-bank matrices, TMA u + LDG geometry)"
         if lx <= 15:
             ring = "one-deep" if lx >= 9 or (lx == 7 and mode == "strict") else "two-deep"

@@ -84,12 +84,12 @@ static cudaError_t launch_line_t(const AxPtrs& A, int64_t nel, cudaStream_t st, 
   return cudaGetLastError();
 }
 
-// Default for lx 9..16, both modes (same-box A/B against v4).
+// Default for lx 9..16, both modes, and lx = 7 fast (same-box A/B against
+// v4, profiles/r02_ab_line_*: at lx 5, 6, 8 and 7 strict v4 / v6 stay ahead).
 bool line_selected(const AxPtrs& A, int64_t nel, int lx, int mode) {
-  if (lx < 9 || lx > 16 || ((uintptr_t)A.u & 15u) != 0) return false;
+  if (lx < 7 || lx == 8 || lx > 16 || ((uintptr_t)A.u & 15u) != 0) return false;
   if (nel * lx * lx >= (int64_t)1 << 31) return false;  // tensor-map row coordinate (int32)
-  (void)mode;
-  return true;
+  return lx >= 9 || mode == AXHELM_FAST;  // lx = 7: fast only
 }
 
 cudaError_t launch_line(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
@@ -100,7 +100,7 @@ cudaError_t launch_line(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStre
 #define AXB_LINE(N) \
   case N:           \
     return fast ? launch_line_t<N, true>(A, nel, st, hm) : launch_line_t<N, false>(A, nel, st, hm);
-    AXB_LINE(9) AXB_LINE(10) AXB_LINE(11) AXB_LINE(12) AXB_LINE(13) AXB_LINE(14) AXB_LINE(15) AXB_LINE(16)
+    AXB_LINE(7) AXB_LINE(9) AXB_LINE(10) AXB_LINE(11) AXB_LINE(12) AXB_LINE(13) AXB_LINE(14) AXB_LINE(15) AXB_LINE(16)
 #undef AXB_LINE
     default:
       return cudaErrorInvalidValue;

@@ -57,11 +57,13 @@ struct LineCfg {
   static constexpr int L3 = LX * LX * LX;
   // elements per CTA-iteration: whole warps are the FP64 pipe's unit, so a
   // group of EPC elements (EPC * lx^2 threads) wastes fewer lanes than one
-  // (lx = 10: 100 of 128 lanes busy, two elements 200 of 224)
+  // (lx = 7: 49 of 64 lanes busy, three elements 147 of 160).  At lx 9..15
+  // two or three elements per CTA measured 0.8-0.95x (fewer CTAs per SM,
+  // profiles/r02_ab_line_epc.txt).
 #ifdef AXL_EPC
   static constexpr int EPC = LX == 16 ? 1 : AXL_EPC;
 #else
-  static constexpr int EPC = 1;
+  static constexpr int EPC = LX == 7 ? 3 : 1;
 #endif
   static constexpr int NT = EPC * L2;
   // X0 / X1 layout [k][j][i]: row stride RS, plane stride PS (doubles);
@@ -116,7 +118,7 @@ struct LineGP {
 #ifdef AXL_MINB_FAST
   static constexpr int MF = AXL_MINB_FAST;
 #else
-  static constexpr int MF = LX <= 12 ? 3 : 2;
+  static constexpr int MF = LX <= 8 ? 0 : LX <= 12 ? 3 : 2;
 #endif
 #ifdef AXL_MINB_STRICT
   static constexpr int MS = AXL_MINB_STRICT;

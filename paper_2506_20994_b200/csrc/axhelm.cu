@@ -76,9 +76,9 @@ static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
 // pf (v2, L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
 // + k-split), dmma (v6, FP64 tensor cores; fast mode, lx = 8) or line (v11,
-// lx >= 9, both modes).  Default ("auto"): v6 for fast lx = 8, v11 for lx
-// 9..16 (u 16-B aligned), v4 for every other lx <= 15 (16-B aligned
-// fields), else v2.  (v3 = v4 without its refinements and v5 = row per
+// lx 7 / 9..16).  Default ("auto"): v6 for fast lx = 8, v11 for lx 9..16
+// and fast lx = 7 (u 16-B aligned), v4 for every other lx <= 15 (16-B
+// aligned fields), else v2.  (v3 = v4 without its refinements and v5 = row per
 // thread were measured and retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
 static int g_variant = [] {
@@ -367,7 +367,7 @@ template <int LX, bool FAST>
 static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm,
                                   const AxExt& X) {
   if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
-  if constexpr (LX >= 9) {
+  if constexpr (LX == 7 || LX >= 9) {
     constexpr int M = FAST ? AXHELM_FAST : AXHELM_STRICT;
     if ((g_variant == 11 && line_selected(A, nel, LX, AXHELM_FAST)) || (g_variant == 0 && line_selected(A, nel, LX, M)))
       return launch_line(A, nel, LX, M, st, hm);

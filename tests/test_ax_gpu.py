@@ -229,15 +229,18 @@ def test_matrix_changed_in_place_is_honoured(torch, kern, lx):
             assert np.array_equal(dev["wd"].cpu().numpy(), o.ax(arrays)), name
 
 
-@pytest.mark.parametrize("lx", range(9, 17))
+@pytest.mark.parametrize("lx", [7] + list(range(9, 17)))
 @pytest.mark.parametrize("mode", ["strict", "fast"])
 def test_line_kernel_many_iterations(torch, kern, lx, mode):
-    """v11 line kernel (lx 9..16): several elements per persistent CTA (the u
+    """v11 line kernel (lx 9..16, lx 7 fast in groups of three elements): several
+    elements per persistent CTA (the u
     buffer re-armed by TMA after stage 1, the mbarrier parity flipping, the
     geometry pipeline and L2 prefetch crossing elements), odd element
     offsets for odd lx^3 and the past-the-end fallback element — strict
     bit-exact, fast within 1e-12."""
     nel = 2600 if lx <= 12 else 1300
+    if lx == 7:
+        nel = 3 * 2600 + 2  # a partial last group
     arrays = o.problem(lx, nel, seed=5 + lx)
     want = o.ax(arrays)
     got = run_dev(torch, kern[mode], arrays, nel, lx)
