@@ -32,8 +32,9 @@
 //           --- barrier;  w = (X0 + X1) + wt at (j=a, i=b), streamed out
 //   strict: the reference adds the three stage-2 terms interleaved per l
 //           (sem.py:332-335), so stage 2 stays a column walk: thread (j,i)
-//           holds dxt[.][i], dyt[.][j] (from the shared copy) and its ut
-//           column, reads ur rows / us j-lines from X0 / X1.
+//           owns the LX outputs of its column and its ut column, reads ur
+//           rows / us j-lines from X0 / X1; l outer, the LX chains side by
+//           side (LineGP::S2LO; k outer at lx 14 / 15).
 // Stage-1 sums (r, s, t each accumulated l-ascending from 0.0) and the
 // combine keep the reference association, so strict output is bit-exact.
 //
@@ -123,7 +124,15 @@ struct LineGP {
 #ifdef AXL_MINB_STRICT
   static constexpr int MS = AXL_MINB_STRICT;
 #else
-  static constexpr int MS = LX <= 12 ? 0 : 2;
+  static constexpr int MS = LX == 9 ? 4 : LX <= 12 ? 0 : 2;
+#endif
+  // strict stage 2 loop order: l outer (all LX chains of the column advance
+  // together) or k outer (one chain at a time, dxt / dyt rows in registers);
+  // profiles/r02_ab_s2_order.txt
+#ifdef AXL_S2_KOUTER
+  static constexpr bool S2LO = false;
+#else
+  static constexpr bool S2LO = !(LX == 14 || LX == 15);
 #endif
   static constexpr int G0 = FAST ? GF : GS;
   static constexpr int GP = G0 < LX ? G0 : LX;
@@ -260,6 +269,8 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
     line_s<LX, FAST, UP>(P, 2, Uv + a * RU + b, PU, t);
   }
   // geometry of the first GP planes: loads in flight across the barrier
+  // (issuing them before stage 1 instead measured 1.0-1.3x slower,
+  // profiles/r02_ab_geom_early.txt)
   constexpr int GP = LineGP<LX, FAST>::GP;
   const int64_t gbase = e * L3 + a * LX + b;
   double gv[GP][7];
@@ -317,6 +328,29 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
     }
   } else {
     __syncthreads();  // ur / us complete
+    if constexpr (LineGP<LX, false>::S2LO) {
+    // l outer, k inner: the LX output chains of the thread's column advance
+    // together (independent DADD chains back to back), and only one entry of
+    // dxt / dyt is live at a time.  Every point still accumulates its three
+    // terms per l, l ascending, from 0.0 — the reference association.
+    double w[LX];
+#pragma unroll
+    for (int k = 0; k < LX; ++k) w[k] = 0.0;
+#pragma unroll
+    for (int l = 0; l < LX; ++l) {
+      const double dxl = __ldg(A.dxt + l * LX + b), dyl = __ldg(A.dyt + l * LX + a);
+#pragma unroll
+      for (int k = 0; k < LX; ++k) {
+        w[k] = madd<false>(w[k], dxl, X0[k * PS + a * RS + l]);
+        w[k] = madd<false>(w[k], dyl, X1[k * PS + l * RS + b]);
+        w[k] = madd<false>(w[k], mat<LX, UP>(P, 5, l, k), t[l]);
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < LX; ++k) stg_stream(wout + k * L2, w[k]);
+    }
+    } else {
     double dxtr[LX], dytr[LX];
 #pragma unroll
     for (int l = 0; l < LX; ++l) {
@@ -333,6 +367,7 @@ __device__ __forceinline__ void element_line(const LParams<LX>& P, const double*
         w = madd<false>(w, mat<LX, UP>(P, 5, l, k), t[l]);
       }
       if (active) stg_stream(wout + k * L2, w);
+    }
     }
   }
 }

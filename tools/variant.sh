@@ -1,0 +1,16 @@
+#!/bin/bash
+# Build a variant of the library with extra nvcc defines for same-box A/B:
+#   tools/variant.sh NAME "-DAXL_X=1 -DAXL_Y=2"  ->  scratch/NAME/libaxhelm_sm100.so
+# Only ax_line.cu / axhelm.cu are recompiled; the other objects are the tree's.
+set -e
+NAME=$1; DEFS=$2
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+SRC=$ROOT/paper_2506_20994_b200/csrc
+W=/tmp/axvar_$NAME
+rm -rf "$W"; mkdir -p "$W/pkg/csrc" "$W/include" "$ROOT/scratch/$NAME"
+cp "$SRC"/*.cu "$SRC"/*.cuh "$SRC"/*.h "$SRC"/Makefile "$W/pkg/csrc/"
+cp "$ROOT"/include/*.h "$W/include/"
+mkdir -p "$W/pkg/csrc/build"; cp "$SRC"/build/*.o "$W/pkg/csrc/build/"
+touch "$W/pkg/csrc/ax_line.cu" "$W/pkg/csrc/axhelm.cu"
+make -C "$W/pkg/csrc" -j4 NVFLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v $DEFS" LIB="$ROOT/scratch/$NAME/libaxhelm_sm100.so" > "$W/make.log" 2>&1 || { tail -30 "$W/make.log"; exit 1; }
+echo "built scratch/$NAME/libaxhelm_sm100.so"
