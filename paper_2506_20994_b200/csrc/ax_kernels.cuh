@@ -158,98 +158,6 @@ __device__ __forceinline__ void stg_w2(double* p, double v0, double v1, const L2
                : "memory");
 }
 
-// v1 k-walk kernel: one CTA per EPB elements.
-template <int LX, bool FAST>
-__global__ void __launch_bounds__(KCfg<LX>::NT)
-ax_kwalk(const AxPtrs A, const int64_t nel) {
-  using C = KCfg<LX>;
-  constexpr int L2 = C::L2, L3 = C::L3, RS = C::RS, SL = C::SL, ES = C::ES;
-  extern __shared__ double smem[];
-  double* sD = smem;                    // [6][LX][LX]
-  double* sU = sD + 6 * L2;             // [EPB][LX][LX][RS]
-  double* sR = sU + C::EPB * ES;
-  double* sS = sR + C::EPB * ES;
-
-  const int tid = threadIdx.x;
-  for (int q = tid; q < L2; q += C::NT) {
-    sD[0 * L2 + q] = A.dx[q];
-    sD[1 * L2 + q] = A.dy[q];
-    sD[2 * L2 + q] = A.dz[q];
-    sD[3 * L2 + q] = A.dxt[q];
-    sD[4 * L2 + q] = A.dyt[q];
-    sD[5 * L2 + q] = A.dzt[q];
-  }
-  const int el = tid / L2;
-  const int p = tid - el * L2;
-  const int j = p / LX;
-  const int i = p - j * LX;
-  const int64_t e = (int64_t)blockIdx.x * C::EPB + el;
-  const bool active = e < nel;
-  const int64_t gbase = e * L3 + p;  // + k*L2
-  double* eU = sU + el * ES;
-  double* eR = sR + el * ES;
-  double* eS = sS + el * ES;
-
-  double ureg[LX];
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    ureg[k] = active ? ldg_stream(A.u + gbase + k * L2) : 0.0;
-    eU[k * SL + j * RS + i] = ureg[k];
-  }
-  __syncthreads();
-
-  double dxr[LX], dyr[LX];
-#pragma unroll
-  for (int l = 0; l < LX; ++l) {
-    dxr[l] = sD[0 * L2 + l * LX + i];
-    dyr[l] = sD[1 * L2 + l * LX + j];
-  }
-
-  double utr[LX];
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    const int64_t g = gbase + k * L2;
-    double h = 0, a11 = 0, a22 = 0, a33 = 0, a12 = 0, a13 = 0, a23 = 0;
-    if (active) {
-      h = ldg_stream(A.h1 + g);
-      a11 = ldg_stream(A.g11 + g);
-      a22 = ldg_stream(A.g22 + g);
-      a33 = ldg_stream(A.g33 + g);
-      a12 = ldg_stream(A.g12 + g);
-      a13 = ldg_stream(A.g13 + g);
-      a23 = ldg_stream(A.g23 + g);
-    }
-    double r = 0.0, s = 0.0, t = 0.0;
-#pragma unroll
-    for (int l = 0; l < LX; ++l) {
-      r = madd<FAST>(r, dxr[l], eU[k * SL + j * RS + l]);
-      s = madd<FAST>(s, dyr[l], eU[k * SL + l * RS + i]);
-      t = madd<FAST>(t, sD[2 * L2 + l * LX + k], ureg[l]);
-    }
-    eR[k * SL + j * RS + i] = combine<FAST>(h, a11, a12, a13, r, s, t);
-    eS[k * SL + j * RS + i] = combine<FAST>(h, a12, a22, a23, r, s, t);
-    utr[k] = combine<FAST>(h, a13, a23, a33, r, s, t);
-  }
-  __syncthreads();
-
-#pragma unroll
-  for (int l = 0; l < LX; ++l) {
-    dxr[l] = sD[3 * L2 + l * LX + i];
-    dyr[l] = sD[4 * L2 + l * LX + j];
-  }
-#pragma unroll
-  for (int k = 0; k < LX; ++k) {
-    double w = 0.0;
-#pragma unroll
-    for (int l = 0; l < LX; ++l) {
-      w = madd<FAST>(w, dxr[l], eR[k * SL + j * RS + l]);
-      w = madd<FAST>(w, dyr[l], eS[k * SL + l * RS + i]);
-      w = madd<FAST>(w, sD[5 * L2 + l * LX + k], utr[l]);
-    }
-    if (active) stg_stream(A.w + gbase + k * L2, w);
-  }
-}
-
 }  // namespace axb
 
 namespace axb {

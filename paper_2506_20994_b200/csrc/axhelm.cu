@@ -54,36 +54,17 @@ int cuda_status(cudaError_t e, const char* where) {
 // per device.  Entries are written once (idempotent, benign race).
 // ---------------------------------------------------------------- launch
 
-template <int LX, bool FAST>
-static cudaError_t launch_kwalk(const AxPtrs& A, int64_t nel, cudaStream_t st) {
-  using C = KCfg<LX>;
-  static DevCache attr_done;
-  const int dev = cur_dev();
-  if (dev < 0) return cudaErrorInvalidDevice;
-  if (!attr_done.v[dev].load(std::memory_order_relaxed)) {
-    cudaError_t e = cudaFuncSetAttribute(ax_kwalk<LX, FAST>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done.v[dev].store(1, std::memory_order_relaxed);
-  }
-  const int64_t blocks = (nel + C::EPB - 1) / C::EPB;
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  ax_kwalk<LX, FAST><<<(unsigned)blocks, C::NT, C::SMEM, st>>>(A, nel);
-  return cudaGetLastError();
-}
-
-// Kernel variant (A/B switch for profiling): AXHELM_KERNEL = kwalk (v1),
-// pf (v2, L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
+// Kernel variant (A/B switch for profiling): AXHELM_KERNEL = pf (v2,
+// L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
 // + k-split), dmma (v6, FP64 tensor cores; fast mode, lx = 8) or line (v11,
 // lx 7 / 9..16).  Default ("auto"): v6 for fast lx = 8, v11 for lx 9..16
 // and fast lx = 7 (u 16-B aligned), v4 for every other lx <= 15 (16-B
-// aligned fields), else v2.  (v3 = v4 without its refinements and v5 = row per
-// thread were measured and retired.)
+// aligned fields), else v2.  (v1 = the k-walk without prefetch, v3 = v4
+// without its refinements and v5 = row per thread were measured and
+// retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
 static int g_variant = [] {
   const char* v = getenv("AXHELM_KERNEL");
-  if (v && !strcmp(v, "kwalk")) return 1;
   if (v && !strcmp(v, "pf")) return 2;
   if (v && !strcmp(v, "tma2")) return 4;
   if (v && !strcmp(v, "dmma")) return 6;
@@ -366,7 +347,6 @@ static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 template <int LX, bool FAST>
 static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm,
                                   const AxExt& X) {
-  if (g_variant == 1) return launch_kwalk<LX, FAST>(A, nel, st);
   if constexpr (LX == 7 || LX >= 9) {
     constexpr int M = FAST ? AXHELM_FAST : AXHELM_STRICT;
     if ((g_variant == 11 && line_selected(A, nel, LX, AXHELM_FAST)) || (g_variant == 0 && line_selected(A, nel, LX, M)))
