@@ -779,7 +779,10 @@ def ours_arm(args):
     # ---- C4 / C5 strong-scaled over the ws ranks, per transport
     c4 = c5 = None
     if not args.no_c4:
-        transports = ["local"] if ws == 1 else (["peer", "nccl"] if xchg == "peer" else ["nccl"])
+        # the collective transport is named after the process group's backend
+        # (gloo when several ranks share one GPU and NCCL cannot run)
+        coll = backend if ws > 1 else "nccl"
+        transports = ["local"] if ws == 1 else (["peer", coll] if xchg == "peer" else [coll])
         res, cmesh = strong_scaled(args, torch, device, comm, ws, rank, timer, transports)
         one = None
         if ws > 1:  # the same 2^21 problem on ONE GPU (rank 0 alone) for the efficiency

@@ -1,9 +1,10 @@
 #!/bin/bash
 # Build a variant of the library with extra nvcc defines for same-box A/B:
-#   tools/variant.sh NAME "-DAXL_X=1 -DAXL_Y=2"  ->  scratch/NAME/libaxhelm_sm100.so
-# Only ax_line.cu / axhelm.cu are recompiled; the other objects are the tree's.
+#   tools/variant.sh NAME "-DAXL_X=1 -DAXL_Y=2" [sources]  ->  scratch/NAME/libaxhelm_sm100.so
+# Only the listed sources (default: ax_line.cu axhelm.cu) are recompiled; the
+# other objects are the tree's.
 set -e
-NAME=$1; DEFS=$2
+NAME=$1; DEFS=$2; SRCS=${3:-"ax_line.cu axhelm.cu"}
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 SRC=$ROOT/paper_2506_20994_b200/csrc
 W=/tmp/axvar_$NAME
@@ -11,6 +12,6 @@ rm -rf "$W"; mkdir -p "$W/pkg/csrc" "$W/include" "$ROOT/scratch/$NAME"
 cp "$SRC"/*.cu "$SRC"/*.cuh "$SRC"/*.h "$SRC"/Makefile "$W/pkg/csrc/"
 cp "$ROOT"/include/*.h "$W/include/"
 mkdir -p "$W/pkg/csrc/build"; cp "$SRC"/build/*.o "$W/pkg/csrc/build/"
-touch "$W/pkg/csrc/ax_line.cu" "$W/pkg/csrc/axhelm.cu"
+for f in $SRCS; do touch "$W/pkg/csrc/$f"; done
 make -C "$W/pkg/csrc" -j4 NVFLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v $DEFS" LIB="$ROOT/scratch/$NAME/libaxhelm_sm100.so" > "$W/make.log" 2>&1 || { tail -30 "$W/make.log"; exit 1; }
 echo "built scratch/$NAME/libaxhelm_sm100.so"
