@@ -8,4 +8,5 @@ for lx in "$@"; do
     python tools/sweep.py --lx $lx --modes $MODE --reps 2 > /dev/null 2>&1
   python tools/ncu_summary.py $R.ncu-rep > $R.txt 2>&1
   python tools/ncu_lines.py $R.ncu-rep 14 >> $R.txt 2>&1
+  [ -n "$KEEP_REP" ] || rm -f $R.ncu-rep  # gpurun copies back <= 64 MiB
 done
