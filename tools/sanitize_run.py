@@ -23,6 +23,17 @@ for lx in (3, 5, 7, 8, 9, 12, 16):
             arr[n] = torch.from_numpy(rng.standard_normal((nel, lx, lx, lx))).cuda()
         arr["wd"] = torch.zeros(nel, lx, lx, lx, dtype=torch.float64, device="cuda")
         load_kernel(mode=mode)(arr, nel, lx)
+# persistent line kernel with more groups than resident CTAs: the u buffer
+# re-armed by TMA, the mbarrier parity flipping, the geometry pipeline and
+# prefetches crossing elements (lx 7: three elements per CTA, partial group)
+for lx, nel in ((7, 1801), (9, 701), (16, 321)):
+    arr = {n: torch.from_numpy(rng.standard_normal((lx, lx))).cuda() for n in
+           ("dxd", "dyd", "dzd", "dxtd", "dytd", "dztd")}
+    for n in ("ud", "h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d"):
+        arr[n] = torch.from_numpy(rng.standard_normal((nel, lx, lx, lx))).cuda()
+    arr["wd"] = torch.zeros(nel, lx, lx, lx, dtype=torch.float64, device="cuda")
+    for mode in ("strict", "fast"):
+        load_kernel(mode=mode)(arr, nel, lx)
 torch.cuda.synchronize()
 for sched in ("sequential", "follow", 1):
     m = BoxMesh(3, 2, 4, 8)
