@@ -484,3 +484,21 @@ def test_concurrent_reference_symbol_calls(torch):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def test_signed_zero_inputs_strict_digest(torch, kern, golden_dir):
+    """Elements whose u is exact +-0.0 (every product +-0): strict output
+    carries the reference's zero signs (digests from sem.ax_reference,
+    tests/golden/make_zero_golden.py), for every kernel family (v4 lx <= 8,
+    v11 line kernel lx >= 9)."""
+    import json
+    import sys
+
+    sys.path.insert(0, str(golden_dir))
+    from make_zero_golden import CASES, zero_inputs
+
+    want = json.loads((golden_dir / "zero_digests.json").read_text())
+    for lx, nel in CASES:
+        arrays = zero_inputs(o.problem(lx, nel))
+        got = run_dev(torch, kern["strict"], arrays, nel, lx)
+        assert o.digest(got) == want[f"{lx},{nel}"]["w"], (lx, nel)

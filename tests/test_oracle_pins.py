@@ -207,3 +207,18 @@ def test_oracle_dssum_and_pcg_pinned_to_reference_assembly(golden_dir):
         if lx <= 5 and np.count_nonzero(np.abs(c["x"]) > 0) > 50:
             x, _ = o.pcg(arrays, gid, mask, c["f"], iters=150)
             assert np.abs(x - c["x"]).max() <= 1e-9 * np.abs(c["x"]).max(), (nx, ny, nz, lx)
+
+
+def test_signed_zero_inputs_pinned(golden_dir):
+    """u with exact zeros of both signs (tests/golden/make_zero_golden.py,
+    digests written by the reference's sem.ax_reference): the oracle's
+    running sums from +0.0 give the reference's zero signs bit for bit."""
+    import sys
+
+    sys.path.insert(0, str(golden_dir))
+    from make_zero_golden import CASES, zero_inputs
+
+    want = json.loads((golden_dir / "zero_digests.json").read_text())
+    for lx, nel in CASES:
+        arrays = zero_inputs(o.problem(lx, nel))
+        assert o.digest(o.ax(arrays)) == want[f"{lx},{nel}"]["w"], (lx, nel)
