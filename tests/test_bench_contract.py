@@ -1,5 +1,6 @@
 """The bench.py JSON contract, checked on the committed bench line
-(profiles/r01_bench_s7.json) and on the argument defaults (CPU only)."""
+(profiles/r02b_bench.json, this round's GPU run) and on the argument
+defaults (CPU only)."""
 
 import json
 import sys
@@ -9,7 +10,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 def test_recorded_bench_line_has_the_contract_keys():
-    d = json.loads((ROOT / "profiles" / "r01_bench_s7.json").read_text())
+    d = json.loads((ROOT / "profiles" / "r02b_bench.json").read_text())
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "cpu_baseline",
               "clocks", "gpu_launches"):
@@ -27,6 +28,24 @@ def test_recorded_bench_line_has_the_contract_keys():
     k = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(k)
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(k["reasons"])
+
+
+def test_recorded_bench_line_round2_blocks():
+    """Round-2 keys: the same-config CPU arm with its parity gates, the C3
+    sweep with a clock record per entry, and C4 / C5 strong-scaled blocks."""
+    d = json.loads((ROOT / "profiles" / "r02b_bench.json").read_text())
+    c = d["cpu_baseline"]
+    assert c["same_config"] is True and c["gate"]["strict_bit_exact"] is True
+    assert c["gate"]["fast_normwise"] <= 1e-12
+    sweep = d["lx_sweep"]
+    assert {(e["lx"], e["mode"]) for e in sweep} == {(lx, m) for lx in range(2, 17) for m in ("fast", "strict")}
+    for e in sweep:
+        assert e["kernel_ms"] > 0 and e["hbm_gbs"] > 0 and {"sm_mhz", "reasons"} <= set(e["clocks"])
+        assert e["c3"] == (e["lx"] <= 12)
+    for key in ("c4", "c5"):
+        b = d[key]
+        assert b["elements_total"] == 1 << 21 and b["scaling"] == "strong" and b["target_efficiency"] == 0.85
+        assert all("parallel_efficiency" in t for t in b["transports"].values())
 
 
 def test_bench_defaults_are_the_headline_configuration():
