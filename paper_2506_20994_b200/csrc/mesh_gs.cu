@@ -356,10 +356,10 @@ __global__ void gs_box_plane_peer_kernel(double* __restrict__ w, const BoxGS M, 
 //  CLS 1: the other planes, rows on y faces (gy % n1 == 0): every gx
 //  CLS 2: the other planes and rows: x-face nodes only (gx = fx * n1)
 // z-plane sets are [zlo, zhi] (inclusive) of node planes owned locally.
-// CLS 0 / 1 threads take NB nodes (consecutive rows / planes) and issue all
-// their loads before any sum (the one-node version was latency-bound at
-// 2-3 TB/s: only 2-4 independent loads per thread); CLS 2 is already
-// sector-bound and stays one node per thread.
+// A thread may take NB nodes (consecutive rows / planes) and issue all
+// their loads before any sum; NB = 1 everywhere since the node-dense
+// enumeration (2 and 4 measured neutral for classes 0 / 1 at 4.2 TB/s,
+// profiles/r02_ab_gs_nb.txt).
 template <int LX, int NB>
 __device__ __forceinline__ void gs_box_local_nodes(double* __restrict__ w, const BoxGS& M,
                                                    const int (&gx)[NB], const int (&gy)[NB],
