@@ -309,7 +309,7 @@ def test_mdg_bench_sweep_on_gpu(tmp_path):
     assert text.splitlines()[0] == mdg_bench.CSV_HEADER and len(text.splitlines()) == 9
 
 
-@pytest.mark.parametrize("lx,nel", [(8, 1 << 18), (12, 57870), (5, 800000)])
+@pytest.mark.parametrize("lx,nel", [(8, 1 << 18), (12, 57870), (5, 800000), (7, 291545), (9, 137174), (16, 24414)])
 def test_full_size_operator_properties(torch, kern, lx, nel):
     """Size-independent properties of A at the sweep / C2 sizes, both modes
     (tests/test_oracle.py:129-135, :175-185, :227-231 restated per element):
