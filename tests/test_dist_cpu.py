@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, nx, ny, nz, lx, q):
+def _worker(rank, world, port, nx, ny, nz, lx, q, staged=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -44,20 +44,27 @@ def _worker(rank, world, port, nx, ny, nz, lx, q):
         wglob = rng.standard_normal((nx * ny * nz, lx, lx, lx))
         want = o.dssum(wglob, o.box_mesh_gid(nx, ny, nz, lx))[ez0 * nx * ny: ez1 * nx * ny]
         w = torch.from_numpy(wglob[ez0 * nx * ny: ez1 * nx * ny].copy())
-        SlabDSSUM(ops, TorchComm(dist))(w)
+        comm = TorchComm(dist)
+        # staged=False: the branch the NCCL backend takes (send / receive the
+        # given tensors directly, no host copies) — gloo moves CPU tensors
+        # the same way, so the message pairing and ordering of the device
+        # path are exercised here
+        comm.host_staged = staged
+        SlabDSSUM(ops, comm)(w)
         q.put((rank, bool(np.array_equal(w.numpy(), want)),
                o.digest(w.numpy()) == o.digest(want)))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("staged", [True, False])
 @pytest.mark.parametrize("world,dims", [(2, (3, 2, 4, 3)), (3, (2, 3, 5, 4)), (2, (2, 2, 2, 8))])
-def test_slab_dssum_gloo_bit_exact(world, dims):
+def test_slab_dssum_gloo_bit_exact(world, dims, staged):
     nx, ny, nz, lx = dims
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, ny, nz, lx, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, ny, nz, lx, q, staged)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
