@@ -1,11 +1,12 @@
-"""Summarise tools/ab.sh output: best time per (lx, mode) for A and B, B/A."""
+"""Summarise tools/ab.sh output: best time per (lx, mode) for A and B, B/A.
+python tools/ab_table.py FILE  (or the output on stdin: tools/ab.sh ... | python tools/ab_table.py)"""
 import collections
 import re
 import sys
 
 cur = None
 res = collections.defaultdict(list)
-for line in sys.stdin:
+for line in (open(sys.argv[1]) if len(sys.argv) > 1 else sys.stdin):
     if line.startswith("=="):
         cur = line.split()[1]
         continue
