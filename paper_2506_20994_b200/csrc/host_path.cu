@@ -22,6 +22,8 @@
 #include <thread>
 #include <vector>
 
+#include <emmintrin.h>  // SSE2 streaming stores (x86-64 baseline)
+
 #include "../../include/axhelm.h"
 #include "ax_launch.h"
 
@@ -57,6 +59,8 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 // -> 53.6 GB/s = 96% of the 55.6 GB/s raw pinned copy)
 const int NS = env_int("AXHELM_STAGE_SLOTS", 4, 2, NS_MAX);
 const int64_t CHUNK_PTS = env_int("AXHELM_STAGE_CHUNK", 1 << 22, 1 << 12, 1 << 26);
+// chunk when some argument is pageable (host-thread staging copies)
+const int64_t CHUNK_PTS_PAGEABLE = env_int("AXHELM_STAGE_CHUNK_PAGEABLE", 1 << 20, 1 << 12, 1 << 26);
 
 // A small pool of host threads for parallel memcpy (pageable <-> pinned).
 class CopyPool {
@@ -110,12 +114,40 @@ class CopyPool {
   bool stop_ = false;
 };
 
+// one thread's part of a staging copy.  Non-temporal (streaming) stores: the
+// destination is written once and read by the copy engine or the caller
+// later, so skipping the read-for-ownership of every destination line cuts
+// the host-memory traffic of the copy from three passes to two (the copy
+// engines share that bandwidth).  sfence: the stores are visible before the
+// pool reports the part done.
+void stage_copy(double* dst, const double* src, int64_t n) {
+#ifdef AX_NO_NT_COPY
+  memcpy(dst, src, sizeof(double) * (size_t)n);
+#else
+  int64_t i = 0;
+  if (((uintptr_t)dst & 15u) && n > 0) {
+    dst[0] = src[0];
+    i = 1;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m128d v0 = _mm_loadu_pd(src + i), v1 = _mm_loadu_pd(src + i + 2);
+    const __m128d v2 = _mm_loadu_pd(src + i + 4), v3 = _mm_loadu_pd(src + i + 6);
+    _mm_stream_pd(dst + i, v0);
+    _mm_stream_pd(dst + i + 2, v1);
+    _mm_stream_pd(dst + i + 4, v2);
+    _mm_stream_pd(dst + i + 6, v3);
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+#endif
+}
+
 // copy n doubles src -> dst with every pool thread taking a contiguous part
 void par_copy(CopyPool& pool, double* dst, const double* src, int64_t n) {
   const int T = pool.size();
   pool.run([&](int i) {
     const int64_t a = n * i / T, b = n * (i + 1) / T;
-    if (b > a) memcpy(dst + a, src + a, sizeof(double) * (size_t)(b - a));
+    if (b > a) stage_copy(dst + a, src + a, b - a);
   });
 }
 
@@ -218,7 +250,7 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
   // in 1 Mi-point chunks (C2: 235 -> 215 ms; pinned keeps 4 Mi: 51.5 -> 53.6 GB/s)
   bool pageable_args = false;
   for (int q = 0; q < 15; ++q) pageable_args |= kind[q] == PAGEABLE;
-  const int64_t chunk_pts = pageable_args ? (CHUNK_PTS < (1 << 20) ? CHUNK_PTS : (1 << 20)) : CHUNK_PTS;
+  const int64_t chunk_pts = pageable_args ? CHUNK_PTS_PAGEABLE : CHUNK_PTS;
   const int64_t chunk_el0 = chunk_pts / L3 > 0 ? chunk_pts / L3 : 1;
   const int64_t chunk_el = nel < chunk_el0 ? nel : chunk_el0;
   if ((e = ensure(S, chunk_el * L3)) != cudaSuccess) return cuda_status(e, "__dace_ax_helm (staging setup)");
@@ -280,8 +312,7 @@ int host_or_device_apply(const double* const ptrs[15], int64_t nel, int lx, int 
         S.pool->run([&](int i) {
           const int64_t a = n * i / T, b = n * (i + 1) / T;
           if (b <= a) return;
-          for (int k = 0; k < nq; ++k)
-            memcpy(hslot + (size_t)qs[k] * PP + a, ptrs[fidx[qs[k]]] + off + a, sizeof(double) * (size_t)(b - a));
+          for (int k = 0; k < nq; ++k) stage_copy(hslot + (size_t)qs[k] * PP + a, ptrs[fidx[qs[k]]] + off + a, b - a);
         });
       }
     }
