@@ -401,7 +401,6 @@ def self_launch(args):
            str(ROOT / "bench.py")] + sys.argv[1:]
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only rank 0's JSON line
     env.setdefault("OMP_NUM_THREADS", "1")
     return subprocess.call(cmd, env=env)
 
@@ -418,10 +417,6 @@ def init_dist(torch, ws, local):
     if ndev:
         torch.cuda.set_device(local % ndev)
     if backend == "nccl":
-        # NCCL's init log (ranks, transports, NVLS) on stderr also when the
-        # driver launches torchrun itself; stdout stays one JSON line
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
     else:
         dist.init_process_group(backend)
