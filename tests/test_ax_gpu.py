@@ -502,3 +502,20 @@ def test_signed_zero_inputs_strict_digest(torch, kern, golden_dir):
         arrays = zero_inputs(o.problem(lx, nel))
         got = run_dev(torch, kern["strict"], arrays, nel, lx)
         assert o.digest(got) == want[f"{lx},{nel}"]["w"], (lx, nel)
+
+
+@pytest.mark.parametrize("lx", range(2, 17))
+def test_random_sizes_and_seeds(torch, kern, lx):
+    """Ragged element counts (1, primes, one past a CTA group / ring
+    boundary) and fresh seeds at every lx, every kernel family the
+    dispatcher picks: strict bit-exact against the oracle, fast within the
+    relaxed bar."""
+    rng = np.random.default_rng(1000 + lx)
+    sizes = {1, 2, 3, 7, 13, int(rng.integers(20, 90))}
+    if lx <= 8:
+        sizes |= {149, 297}
+    for nel in sorted(sizes):
+        arrays = o.problem(lx, nel, seed=int(rng.integers(1 << 30)))
+        want = o.ax(arrays)
+        assert o.digest(run_dev(torch, kern["strict"], arrays, nel, lx)) == o.digest(want), (lx, nel)
+        assert o.normwise_rel(run_dev(torch, kern["fast"], arrays, nel, lx), want) <= FAST_TOL, (lx, nel)
