@@ -26,7 +26,7 @@ for lx in (3, 5, 7, 8, 9, 12, 16):
 # persistent line kernel with more groups than resident CTAs: the u buffer
 # re-armed by TMA, the mbarrier parity flipping, the geometry pipeline and
 # prefetches crossing elements (lx 7: three elements per CTA, partial group)
-for lx, nel in ((7, 1801), (9, 701), (16, 321)):
+for lx, nel in ((7, 1801), (9, 701), (10, 601), (16, 321)):
     arr = {n: torch.from_numpy(rng.standard_normal((lx, lx))).cuda() for n in
            ("dxd", "dyd", "dzd", "dxtd", "dytd", "dztd")}
     for n in ("ud", "h1d", "g11d", "g22d", "g33d", "g12d", "g13d", "g23d"):
