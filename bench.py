@@ -63,6 +63,8 @@ ABI = ("wd", "ud", "dxd", "dyd", "dzd", "dxtd", "dytd", "dztd",
 C4_DIMS = (128, 128, 128)  # 2^21 elements: configs C4 / C5
 SWEEP_LX = tuple(range(2, 17))  # C3 is lx 2..12; 13..16 reported beside it
 SAMPLE_NEL = 1 << 15  # the round-1 bounded sample, kept as an extra key
+# (lx, mode) pairs the library runs on the v12 warp-specialised kernel (ax_line.cu WsPick)
+WS_PICKS = {(9, "fast"), (10, "fast")}
 
 
 def flops_model(lx, nel):
@@ -332,6 +334,8 @@ def kernel_name(lx, mode):
     if v == "auto":
         if lx == 8 and mode == "fast":
             return "ax_dmma8 (FP64 DMMA m8n8k4, TMA ring)"
+        if (lx, mode) in WS_PICKS:
+            return f"ax_ws<{lx},{mode}> (line contractions, warp-specialised TMA geometry ring)"
         if lx >= 9 or (lx == 7 and mode == "fast"):
             return f"ax_line<{lx},{mode}> (line contractions, constant-bank matrices, TMA u + LDG geometry)"
         if lx <= 15:

@@ -63,6 +63,11 @@ cudaError_t host_matrices(const AxPtrs& A, int lx, const double* const* hm, cuda
 bool line_selected(const AxPtrs& A, int64_t nel, int lx, int mode);
 cudaError_t launch_line(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
                         const double* const* hm);
+// v12 warp-specialised line kernel (ax_ws.cuh), lx 9 / 10: the default for
+// fast mode (forced: both modes)
+bool ws_selected(const AxPtrs& A, int64_t nel, int lx, int mode, bool forced);
+cudaError_t launch_ws(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
+                      const double* const* hm);
 
 int set_status(int st, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);

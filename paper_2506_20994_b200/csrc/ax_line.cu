@@ -9,6 +9,7 @@
 #include "../../include/axhelm.h"
 #include "ax_launch.h"
 #include "ax_line.cuh"
+#include "ax_ws.cuh"
 
 namespace axb {
 
@@ -82,6 +83,71 @@ static cudaError_t launch_line_t(const AxPtrs& A, int64_t nel, cudaStream_t st, 
   if (grid > groups) grid = groups;
   ax_line<LX, FAST><<<(unsigned)grid, C::NT, C::SMEM, st>>>(P);
   return cudaGetLastError();
+}
+
+// v12 warp-specialised variant (ax_ws.cuh), lx 9 / 10: one CTA per SM.
+// WsPick: consumer groups NG and planes per ring chunk G; the default for
+// fast mode, where it beats v11 on the same box (profiles/r02_ab_ws_kernel.txt:
+// lx 9 1.07x, lx 10 1.06x); strict keeps v11 (AXHELM_KERNEL=ws forces v12
+// for both modes, =line forces v11).
+template <int LX, bool FAST>
+struct WsPick {
+  static constexpr bool ON = FAST;
+  static constexpr int NG = LX == 9 ? 3 : 2;
+  static constexpr int G = LX == 9 ? 9 : 4;
+};
+
+template <int LX, bool FAST>
+static cudaError_t launch_ws_t(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm) {
+  constexpr int NG = WsPick<LX, FAST>::NG, G = WsPick<LX, FAST>::G;
+  using W = WsCfg<LX, NG, G>;
+  static DevCache occ;
+  int blocks_per_sm = 0;
+  cudaError_t e = ctas_per_sm(occ, ax_ws<LX, FAST, NG, G>, W::NT, W::SMEM, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
+  LParams<LX> P;
+  P.A = A;
+  P.nel = nel;
+  P.pf = -1;
+  memset(&P.tmap, 0, sizeof P.tmap);
+  double m6[6 * LX * LX];
+  bool have = false;
+  if ((e = host_matrices(A, LX, hm, st, m6, &P.stale, &have)) != cudaSuccess) return e;
+  if (have) {
+    memcpy(P.m, m6, sizeof P.m);
+  } else {
+    const long long bits = 0x7ff4deadbeef0001LL;
+    double poison;
+    memcpy(&poison, &bits, sizeof poison);
+    for (int q = 0; q < 6 * LX * LX; ++q) (&P.m[0][0])[q] = poison;
+  }
+  int64_t grid = (int64_t)num_sms();
+  if (grid > nel) grid = nel;
+  ax_ws<LX, FAST, NG, G><<<(unsigned)grid, W::NT, W::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+// forced: v12 for lx 9 / 10 in both modes (AXHELM_KERNEL=ws); else WsPick
+bool ws_selected(const AxPtrs& A, int64_t nel, int lx, int mode, bool forced) {
+  if ((lx != 9 && lx != 10) || ((uintptr_t)A.u & 15u) != 0 || nel <= 0) return false;
+  if (forced) return true;
+  const bool fast = mode == AXHELM_FAST;
+  return lx == 9 ? (fast ? WsPick<9, true>::ON : WsPick<9, false>::ON)
+                 : (fast ? WsPick<10, true>::ON : WsPick<10, false>::ON);
+}
+
+cudaError_t launch_ws(const AxPtrs& A, int64_t nel, int lx, int mode, cudaStream_t st,
+                      const double* const* hm) {
+  const bool fast = mode == AXHELM_FAST;
+  switch (lx) {
+#define AXB_WS(N) \
+  case N:         \
+    return fast ? launch_ws_t<N, true>(A, nel, st, hm) : launch_ws_t<N, false>(A, nel, st, hm);
+    AXB_WS(9) AXB_WS(10)
+#undef AXB_WS
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 // Default for lx 9..16, both modes, and lx = 7 fast (same-box A/B against

@@ -56,10 +56,11 @@ int cuda_status(cudaError_t e, const char* where) {
 
 // Kernel variant (A/B switch for profiling): AXHELM_KERNEL = pf (v2,
 // L2-prefetching k-walk), tma2 (v4, TMA ring + constant-bank dz/dzt
-// + k-split), dmma (v6, FP64 tensor cores; fast mode, lx = 8) or line (v11,
-// lx 7 / 9..16).  Default ("auto"): v6 for fast lx = 8, v11 for lx 9..16
-// and fast lx = 7 (u 16-B aligned), v4 for every other lx <= 15 (16-B
-// aligned fields), else v2.  (v1 = the k-walk without prefetch, v3 = v4
+// + k-split), dmma (v6, FP64 tensor cores; fast mode, lx = 8), line (v11,
+// lx 7 / 9..16) or ws (v12, lx 9 / 10).  Default ("auto"): v6 for fast lx
+// = 8, v12 for fast lx 9 / 10, v11 for the other lx 9..16 and fast lx = 7
+// (u 16-B aligned), v4 for every other lx <= 15 (16-B aligned fields), else
+// v2.  (v1 = the k-walk without prefetch, v3 = v4
 // without its refinements and v5 = row per thread were measured and
 // retired.)
 // AXHELM_PF (1..3, lx = 8 only) sets v2's prefetch distance in groups.
@@ -69,6 +70,7 @@ static int g_variant = [] {
   if (v && !strcmp(v, "tma2")) return 4;
   if (v && !strcmp(v, "dmma")) return 6;
   if (v && !strcmp(v, "line")) return 11;
+  if (v && !strcmp(v, "ws")) return 12;
   return 0;  // auto
 }();
 static int g_pf = [] {
@@ -347,6 +349,11 @@ static cudaError_t launch_pf(const AxPtrs& A, int64_t nel, cudaStream_t st) {
 template <int LX, bool FAST>
 static cudaError_t launch_variant(const AxPtrs& A, int64_t nel, cudaStream_t st, const double* const* hm,
                                   const AxExt& X) {
+  if constexpr (LX == 9 || LX == 10) {
+    constexpr int M = FAST ? AXHELM_FAST : AXHELM_STRICT;
+    if ((g_variant == 12 || g_variant == 0) && ws_selected(A, nel, LX, M, g_variant == 12))
+      return launch_ws(A, nel, LX, M, st, hm);
+  }
   if constexpr (LX == 7 || LX >= 9) {
     constexpr int M = FAST ? AXHELM_FAST : AXHELM_STRICT;
     if ((g_variant == 11 && line_selected(A, nel, LX, AXHELM_FAST)) || (g_variant == 0 && line_selected(A, nel, LX, M)))

@@ -519,3 +519,40 @@ def test_random_sizes_and_seeds(torch, kern, lx):
         want = o.ax(arrays)
         assert o.digest(run_dev(torch, kern["strict"], arrays, nel, lx)) == o.digest(want), (lx, nel)
         assert o.normwise_rel(run_dev(torch, kern["fast"], arrays, nel, lx), want) <= FAST_TOL, (lx, nel)
+
+
+@pytest.mark.parametrize("kernel", ["line", "ws"])
+def test_forced_kernel_families_lx9_10(kernel):
+    """The dispatcher runs v12 (warp-specialised) for fast lx 9 / 10 and v11
+    for strict; AXHELM_KERNEL forces one family for both modes (read when
+    the library loads, hence a subprocess): each checked at lx 9 / 10 in
+    both modes over ragged sizes, strict bit-exact, fast 1e-12."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, AXHELM_KERNEL=kernel)
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import oracle as o\n"
+        "from paper_2506_20994_b200 import load_kernel\n"
+        "k = {m: load_kernel(mode=m) for m in ('strict', 'fast')}\n"
+        "for lx in (9, 10):\n"
+        "    for nel in (1, 2, 5, 149, 300, 1001):\n"
+        "        a = o.problem(lx, nel, seed=lx * 1000 + nel)\n"
+        "        want = o.ax(a)\n"
+        "        for m in ('strict', 'fast'):\n"
+        "            d = {kk: torch.from_numpy(np.ascontiguousarray(v)).cuda() for kk, v in a.items()}\n"
+        "            d['wd'].fill_(float('nan'))\n"
+        "            k[m](d, nel, lx)\n"
+        "            got = d['wd'].cpu().numpy()\n"
+        "            if m == 'strict':\n"
+        "                assert o.digest(got) == o.digest(want), (lx, nel, m)\n"
+        "            else:\n"
+        "                assert o.normwise_rel(got, want) <= 1e-12, (lx, nel, m)\n"
+        "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=str(root), env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]

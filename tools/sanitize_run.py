@@ -23,7 +23,8 @@ for lx in (3, 5, 7, 8, 9, 12, 16):
             arr[n] = torch.from_numpy(rng.standard_normal((nel, lx, lx, lx))).cuda()
         arr["wd"] = torch.zeros(nel, lx, lx, lx, dtype=torch.float64, device="cuda")
         load_kernel(mode=mode)(arr, nel, lx)
-# persistent line kernel with more groups than resident CTAs: the u buffer
+# persistent line kernels (v11; v12 for fast lx 9 / 10) with more groups than
+# resident CTAs: the u buffer
 # re-armed by TMA, the mbarrier parity flipping, the geometry pipeline and
 # prefetches crossing elements (lx 7: three elements per CTA, partial group)
 for lx, nel in ((7, 1801), (9, 701), (10, 601), (16, 321)):
