@@ -17,7 +17,7 @@
 // field) into a ring of NS chunks that fills the shared memory left.  The
 // producer runs as far ahead as the ring allows in every phase, so the HBM
 // stream no longer stops while the groups compute; the combine reads its
-// geometry from shared memory.  (NG, G) per lx and mode: WsPick in
+// geometry from shared memory.  (NG, G) per lx: WsPick in
 // ax_line.cu, chosen by same-box A/B (profiles/r02_ab_ws_kernel.txt).
 //
 //   uFull[g] / uEmpty[g]: group g's u buffer (arrive after stage 1)
@@ -39,7 +39,6 @@ struct WsCfg {
   using C = LineCfg<LX>;
   static constexpr int L2 = LX * LX, L3 = L2 * LX;
   static constexpr int GT = (L2 + 31) / 32 * 32;  // threads per consumer group
-  static constexpr int WPG = GT / 32;
   static constexpr int NG = NG_;                  // consumer groups
   static constexpr int NT = NG * GT + 32;         // the groups + the producer warp
   static constexpr int US = (L3 + 2 + 1) & ~1;    // u superset (odd lx^3: one pad double)
