@@ -20,7 +20,8 @@
 // geometry from shared memory.  (NG, G) per lx: WsPick in
 // ax_line.cu, chosen by same-box A/B (profiles/r02_ab_ws_kernel.txt).
 //
-//   uFull[g] / uEmpty[g]: group g's u buffer (arrive after stage 1)
+//   uFull[u] / uEmpty[u]: u buffer u = g * UB + (the group's element count
+//                         mod UB) (arrive after stage 1)
 //   full[s] / empty[s]:   ring slot s (one arrive per consumer thread)
 //   chunk c of the CTA's j-th element (j-th in blockIdx + j*grid order):
 //   q = j*NC + c  ->  slot q % NS, use q / NS (NS a multiple of NG*NC: a
@@ -51,7 +52,11 @@ struct WsCfg {
   static constexpr int SL = (G * L2 + 2 + 1) & ~1;  // ring field slot (16-B superset)
   static constexpr int PLANE = 7 * SL;            // doubles per ring slot
   static constexpr size_t HEAD = 1024;            // mbarriers
-  static constexpr size_t FIXED = HEAD + 8 * (size_t)(NG * US + 2 * NG * XS);
+  // u buffers per group: two let the producer land the group's next u while
+  // the group still works on the current one (1.01-1.02x,
+  // profiles/r02_ab_ws_kernel.txt)
+  static constexpr int UB = 2;
+  static constexpr size_t FIXED = HEAD + 8 * (size_t)(UB * NG * US + 2 * NG * XS);
   static constexpr size_t BUDGET = 227 * 1024;
   static constexpr int NS0 = (int)((BUDGET - FIXED) / (8 * (size_t)PLANE));
   // Ring slots: a multiple of NG * NC, so chunk q and chunk q + NS (the next
@@ -211,19 +216,20 @@ __global__ void __launch_bounds__(WsCfg<LX, NG, G>::NT, 1) ax_ws(const __grid_co
   using W = WsCfg<LX, NG, G>;
   constexpr int L2 = W::L2, L3 = W::L3, NS = W::NS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NU = W::UB * NG;  // u buffers: group g, buffer b -> g * UB + b
   uint64_t* uFull = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* uEmpty = uFull + NG;
-  uint64_t* full = uFull + 2 * NG;
+  uint64_t* uEmpty = uFull + NU;
+  uint64_t* full = uFull + 2 * NU;
   uint64_t* empty = full + NS;
   double* U = reinterpret_cast<double*>(smem_raw + W::HEAD);
-  double* X = U + NG * W::US;
+  double* X = U + NU * W::US;
   double* R = X + 2 * NG * W::XS;
 
   const AxPtrs& A = P.A;
   const int64_t nel = P.nel, grid = gridDim.x;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int g = 0; g < NG; ++g) {
+    for (int g = 0; g < NU; ++g) {
       mbar_init(&uFull[g], 1);
       mbar_init(&uEmpty[g], 1);
     }
@@ -247,17 +253,19 @@ __global__ void __launch_bounds__(WsCfg<LX, NG, G>::NT, 1) ax_ws(const __grid_co
       for (int64_t j = 0; j < nmine; ++j) {
         const int64_t e = blockIdx.x + j * grid;
         const int g = (int)(j % NG);
-        const int64_t use = j / NG;
-        if (use > 0) mbar_wait(&uEmpty[g], (uint32_t)((use - 1) & 1));
+        const int64_t gu = j / NG;                        // the group's element count
+        const int ub = g * W::UB + (int)(gu % W::UB);     // its u buffer
+        const int64_t use = gu / W::UB;                   // that buffer's use count
+        if (use > 0) mbar_wait(&uEmpty[ub], (uint32_t)((use - 1) & 1));
         fence_proxy_async();
         const int64_t first = e * L3;
         const int64_t lo = first & ~(int64_t)1, hi = (first + L3 + 1) & ~(int64_t)1;
         if (hi > nel * L3) {
-          mbar_arrive(&uFull[g]);  // past the end: the group loads u itself
+          mbar_arrive(&uFull[ub]);  // past the end: the group loads u itself
         } else {
           const uint32_t bytes = (uint32_t)((hi - lo) * 8);
-          mbar_arrive_expect_tx(&uFull[g], bytes);
-          bulk_g2s(U + g * W::US, A.u + lo, bytes, &uFull[g]);
+          mbar_arrive_expect_tx(&uFull[ub], bytes);
+          bulk_g2s(U + ub * W::US, A.u + lo, bytes, &uFull[ub]);
         }
         for (int c = 0; c < W::NC; ++c) {
           const int64_t q = j * W::NC + c;  // chunk number in production order
@@ -286,12 +294,15 @@ __global__ void __launch_bounds__(WsCfg<LX, NG, G>::NT, 1) ax_ws(const __grid_co
   const int g = tid / W::GT, tg = tid - g * W::GT;
   const bool act = tg < L2;
   const int a = act ? tg / LX : 0, b = act ? tg - (tg / LX) * LX : 0;
-  double* Ug = U + g * W::US;
+
   double* X0 = X + (2 * g) * W::XS;
   double* X1 = X0 + W::XS;
   for (int64_t j = g; j < nmine; j += NG) {
     const int64_t e = blockIdx.x + j * grid;
-    mbar_wait(&uFull[g], (uint32_t)((j / NG) & 1));
+    const int64_t gu = j / NG;
+    const int ub = g * W::UB + (int)(gu % W::UB);
+    double* Ug = U + ub * W::US;
+    mbar_wait(&uFull[ub], (uint32_t)((gu / W::UB) & 1));
     const int64_t first = e * L3;
     int pad = (int)(first & 1);
     if (((first + L3 + 1) & ~(int64_t)1) > nel * L3) {  // fallback: load u ourselves
@@ -300,9 +311,9 @@ __global__ void __launch_bounds__(WsCfg<LX, NG, G>::NT, 1) ax_ws(const __grid_co
       group_sync(g, W::GT);
     }
     if (use_param)
-      ws_element<LX, FAST, true, NG, G>(P, g, tg, act, a, b, e, j, Ug + pad, X0, X1, &uEmpty[g], full, empty, R);
+      ws_element<LX, FAST, true, NG, G>(P, g, tg, act, a, b, e, j, Ug + pad, X0, X1, &uEmpty[ub], full, empty, R);
     else
-      ws_element<LX, FAST, false, NG, G>(P, g, tg, act, a, b, e, j, Ug + pad, X0, X1, &uEmpty[g], full, empty, R);
+      ws_element<LX, FAST, false, NG, G>(P, g, tg, act, a, b, e, j, Ug + pad, X0, X1, &uEmpty[ub], full, empty, R);
   }
 }
 
