@@ -1,5 +1,5 @@
 """The bench.py JSON contract, checked on the committed bench line
-(profiles/r02d_bench.json, this round's GPU run) and on the argument
+(profiles/r02f_bench.json, this round's GPU run) and on the argument
 defaults (CPU only)."""
 
 import json
